@@ -1,0 +1,313 @@
+"""bench.py — HPL FP64 TFLOP/s on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                    [--n N] [--nb NB] [--no-e2e]
+
+A "step" is one full HPL solve (hpl_factor + hpl_solve: every §8(a) row of
+SURVEY.md runs inside it) of the seeded system at the workload size; the
+matrix is regenerated on the device between steps (untimed, HPL convention:
+generation and the residual check are outside the timing window).  Every
+step's scaled residual must be < 16 or the run fails.  Timing: CUDA events on
+the library's own streams around factor and solve (hpl_last_timing), summed
+over the K steps, max over ranks; inputs (137 GB at the default size) are far
+larger than L2.
+
+Default workload at N=1: BASELINE.json configs[2], N=131072 NB=512 on one B200
+(the largest single-GPU configuration; configs[1] N=8192 is a parity case).
+
+--impl reference: the CPU oracle (oracle/, plain GEPP) timed on this box's host
+cores on a bounded sample of the same workload (a full solve at --cpu-n).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_DERIVED = 148 * 128 * 1965e6 / 1e12  # SMs x FP64 flop/clk x max SM clock (TFLOP/s)
+
+
+def hpl_flops(n: int) -> float:
+    return 2.0 / 3.0 * n ** 3 + 1.5 * n ** 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--n", type=int, default=131072)
+    ap.add_argument("--nb", type=int, default=512)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--cpu-n", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        under = [x for x in sm if x > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(under) if under else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(n: int, seed: int, reps: int = 1):
+    """The oracle (plain GEPP + solves) on the host cores: factor+solve of the
+    seeded N=n system; returns (TFLOP/s, seconds, threads, resid)."""
+    import oracle
+    best = None
+    for _ in range(reps):
+        A, b = oracle.generate(seed, n)
+        t0 = time.perf_counter()
+        LU, ipiv, info = oracle.getrf(A)
+        x = oracle.getrs(LU, ipiv, b)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    r, _ = oracle.residual_seeded(n, seed, x)
+    return hpl_flops(n) / best / 1e12, best, oracle.num_threads(), r
+
+
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the oracle, timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    for _ in range(a.warmup):
+        cpu_baseline(min(a.cpu_n, 1024), a.seed)
+    times = []
+    for _ in range(a.steps):
+        tf, dt, thr, r = cpu_baseline(a.cpu_n, a.seed)
+        if not r < 16.0:
+            print(json.dumps({"impl": "reference", "error": f"oracle residual {r}"}))
+            return 1
+        times.append(dt)
+    T = sum(times)
+    value = a.steps * hpl_flops(a.cpu_n) / T / 1e12
+    line = {
+        "impl": "reference",
+        "metric": "HPL FP64 TFLOP/s (residual<16)", "value": value, "unit": "TFLOP/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * T / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
+        "config": {"workload": f"HPL N={a.n} NB={a.nb} 1x1", "sample": f"full solve at N={a.cpu_n}",
+                   "N": a.n, "NB": a.nb, "grid": "1x1", "l2": "inputs > L2"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+                         "sample": f"oracle GEPP+solves, full solve at N={a.cpu_n} "
+                                   f"(bounded sample of the N={a.n} workload), {cpu_model()}"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import numpy as np
+    import torch
+    import paper_2304_10397_b200 as H
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def allmax(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    N, NB = a.n, a.nb
+    # Multi-GPU: independent per-GPU systems until the P x Q path lands.
+    ctx = H.hpl_init(N, NB, 1, 1, a.seed + rank)
+    H.hpl_set_timing(ctx, True)
+    peak_meas = H.hplk_dmma_peak()
+
+    fl = hpl_flops(N)
+    resids = []
+
+    def step():
+        H.hpl_regenerate(ctx)
+        barrier()
+        H.hpl_factor(ctx)
+        H.hpl_solve(ctx, want_x=False)
+        barrier()
+        t = H.hpl_last_timing(ctx)
+        r = H.hpl_residual(ctx)
+        if not r < 16.0:
+            raise SystemExit(f"rank {rank}: HPL residual {r} >= 16 (FAILED)")
+        resids.append(r)
+        return t
+
+    for _ in range(a.warmup):
+        step()
+    clocks = Clocks(local)
+    clocks.start()
+    tims = [step() for _ in range(a.steps)]
+    ck = clocks.stop()
+    dev_ms = sum(t["factor_ms"] + t["solve_ms"] for t in tims)
+    dev_ms = allmax(dev_ms)
+    dg_ms = sum(t["dgemm_ms"] for t in tims)
+    dg_fl = sum(t["dgemm_flop"] for t in tims)
+    dg_n = sum(t["dgemm_launches"] for t in tims)
+    launches = sum(t["launches"] for t in tims) // max(1, a.steps)
+    value = world * a.steps * fl / (dev_ms * 1e-3) / 1e12
+    dg_tf = dg_fl / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None
+
+    # ---- end to end through the public API with host buffers (pinned)
+    e2e = None
+    if not a.no_e2e:
+        rows, cols = ctx.local_shape
+        try:
+            host_t = torch.empty((rows, cols), dtype=torch.float64, pin_memory=True)
+            pinned = True
+        except Exception:
+            host_t = torch.empty((rows, cols), dtype=torch.float64)
+            pinned = False
+        host = host_t.numpy()
+        H.hpl_regenerate(ctx)
+        ctx.check(H.hpl.lib.hpl_get_local(ctx.h, H.hpl.ptr(host), cols))
+        xh = torch.empty(N, dtype=torch.float64, pin_memory=pinned).numpy()
+        barrier()
+        t0 = time.perf_counter()
+        ctx.check(H.hpl.lib.hpl_load_local(ctx.h, H.hpl.ptr(host), cols))
+        H.hpl_factor(ctx)
+        ctx.check(H.hpl.lib.hpl_solve(ctx.h, H.hpl.ptr(xh)))
+        barrier()
+        dt = allmax(time.perf_counter() - t0)
+        r = H.hpl_residual(ctx)
+        if not r < 16.0:
+            raise SystemExit(f"e2e residual {r} >= 16")
+        e2e = {"value": world * fl / dt / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(rows * cols * 8), "d2h_bytes_per_step": int(N * 8),
+               "pinned": pinned, "s": dt}
+        del host_t
+
+    cpu = None
+    if rank == 0 and not a.no_cpu:
+        tf, dt, thr, rr = cpu_baseline(a.cpu_n, a.seed)
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+               "sample": f"oracle GEPP+solves, full solve at N={a.cpu_n} ({dt:.1f} s; bounded "
+                         f"sample of the N={N} workload), {cpu_model()}", "resid": rr}
+
+    traffic = None
+    tf_path = os.path.join(ROOT, "profiles", "dgemm_traffic.json")
+    if os.path.exists(tf_path):
+        try:
+            traffic = json.load(open(tf_path)).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    H.hpl_free(ctx)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": "HPL FP64 TFLOP/s (residual<16)",
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": dev_ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
+        "config": {"workload": f"HPL N={N} NB={NB} 1x1 per GPU", "N": N, "NB": NB,
+                   "grid": "1x1", "parallelism": "1 GPU" if world == 1 else
+                   f"{world} independent 1x1 systems (P x Q path not built yet)",
+                   "lookahead": True, "l2": "inputs (137 GB) >> L2, no flush needed",
+                   "residual_max": max(resids), "frac_of_fp64_peak": value / world / FP64_PEAK_DERIVED},
+        "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (trailing update)",
+                     "achieved": dg_tf, "peak": FP64_PEAK_DERIVED, "unit": "TFLOP/s",
+                     "frac": (dg_tf / FP64_PEAK_DERIVED) if dg_tf else None,
+                     "traffic": traffic, "launches": dg_n // max(1, a.steps),
+                     "peak_source": "derived 148 SM x 128 FP64 flop/clk x 1965 MHz (MEASURED_PEAKS"
+                                    ".json has no FP64 entry)",
+                     "peak_measured_dmma": peak_meas},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": ck,
+        "impl": "native",
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

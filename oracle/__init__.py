@@ -75,6 +75,8 @@ def lib():
             L.oracle_run.argtypes = [i64, u64, dp, ip, ctypes.POINTER(ctypes.c_double), dp]
             L.oracle_maxloc.restype = i64
             L.oracle_maxloc.argtypes = [i64, dp, ip]
+            L.oracle_residual_rows.restype = None
+            L.oracle_residual_rows.argtypes = [i64, u64, dp, i64, ip, dp, dp]
             L.oracle_num_threads.restype = ctypes.c_int
             L.oracle_num_threads.argtypes = []
             _lib = L
@@ -196,6 +198,16 @@ def run(N: int, seed: int, want_lu: bool = False):
     if want_lu:
         out["LU"] = LU
     return out
+
+
+def residual_rows(N: int, seed: int, x, rows):
+    """(r, rowsum|A0|) for the given global rows of the seeded system."""
+    x = _f64c(x)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    r = np.empty(len(rows), dtype=np.float64)
+    a = np.empty(len(rows), dtype=np.float64)
+    lib().oracle_residual_rows(N, seed, _p(x), len(rows), _p(rows), _p(r), _p(a))
+    return r, a
 
 
 def maxloc(absval, rows):

@@ -301,3 +301,23 @@ int64_t oracle_maxloc(int64_t n, const double *absval, const int64_t *row)
             best = c;
     return best;
 }
+
+/* Sampled residual rows at any N (full-size parity):
+ * r[t] = sum_j A0[rows[t]][j] * x[j] - b0[rows[t]], j ascending, plus the
+ * row sums of |A0| in rsum[t]. */
+void oracle_residual_rows(int64_t N, uint64_t seed, const double *x, int64_t nrows,
+                          const int64_t *rows, double *r, double *rsum)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < nrows; ++t) {
+        const int64_t i = rows[t];
+        double s = 0.0, a = 0.0;
+        for (int64_t j = 0; j < N; ++j) {
+            double v = oracle_gen_entry(seed, N, i, j);
+            s = s + v * x[j];
+            a = a + fabs(v);
+        }
+        r[t] = s - oracle_gen_entry(seed, N, i, N);
+        rsum[t] = a;
+    }
+}

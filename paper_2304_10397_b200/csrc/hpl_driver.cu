@@ -1,0 +1,520 @@
+// hpl_driver.cu — the C ABI (include/hpl.h) and the per-iteration schedule.
+//
+// One iteration j of blocked right-looking LU (SPEC.md glossary l.543–552;
+// PAPER.md l.9 for the look-ahead):
+//   RS/LASWP(j)  : apply panel j's pivots to the trailing columns (gather the
+//                  block row's final rows into U, scatter displaced rows);
+//   DTRSM(j)     : block row j <- L11^{-1} U   (L11^{-1} formed once per panel);
+//   DGEMM(j)     : A22 -= L21 * U12;
+//   FACT(j+1)    : next panel, on the device.
+// Look-ahead depth 1 ("perform the UPDATE phase on only the
+// leading NB columns, and then immediately begin ... while completing the
+// UPDATE phase on the remaining local matrix"): the update of panel j+1's
+// columns and FACT(j+1) run on a high-priority stream S_la while the rest of
+// the trailing update runs on S_tr; events order the two.
+#include "hpl_internal.cuh"
+#include "../../include/hpl.h"
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace hpl;
+
+struct hpl_ctx {
+    // problem
+    int64_t N = 0;
+    int NB = 0, P = 1, Q = 1;
+    uint64_t seed = 0;
+    int rank = 0, nranks = 1, myrow = 0, mycol = 0, device = 0;
+    // local storage
+    int64_t mloc = 0, nloc = 0, lda = 0;
+    double *A = nullptr;
+    double *panel[2] = {nullptr, nullptr};
+    int64_t ldp = 0;
+    double *linv[2] = {nullptr, nullptr};
+    int64_t ldlinv = 0;
+    int64_t *ipiv_rel[2] = {nullptr, nullptr};
+    int64_t *src[2] = {nullptr, nullptr};
+    int64_t *disp[2] = {nullptr, nullptr};
+    int *ndisp[2] = {nullptr, nullptr};
+    int64_t *gpiv = nullptr;
+    double *U = nullptr;     // gathered block rows (pre-DTRSM), NB x ldu
+    double *U2 = nullptr;    // L11^{-1} U (the DGEMM's B operand), NB x ldu
+    int64_t ldu = 0;
+    double *scratch = nullptr;
+    double *x = nullptr, *tbuf = nullptr, *out4 = nullptr;
+    FactWork fw{};
+    cudaStream_t s_la = nullptr, s_tr = nullptr;
+    cudaEvent_t ev_panel[2] = {nullptr, nullptr}, ev_rest = nullptr;
+    // options
+    bool lookahead = true;
+    int nbmin = 16;
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;   // 7 events per iteration when timing
+    std::vector<double> timeline;   // 6 values per iteration (ms)
+    cudaEvent_t ev_t[3] = {nullptr, nullptr, nullptr};  // factor start/end, solve end
+    double factor_ms = 0, solve_ms = 0;
+    double dgemm_ms = 0, dgemm_flop = 0;   // trailing (rest) DGEMM launches, timing on
+    int64_t dgemm_launches = 0;
+    // state
+    enum { S_NONE, S_INIT, S_FACTORED, S_SOLVED } state = S_NONE;
+    std::string err;
+    int64_t singular = -1;
+    int64_t launches = 0;
+};
+
+namespace {
+
+void set_err(hpl_ctx *c, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+}
+
+#define CK(ctx, expr)                                                                       \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess) {                                                            \
+            set_err(ctx, "%s:%d %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+            return HPL_ERR_CUDA;                                                            \
+        }                                                                                   \
+    } while (0)
+
+// numroc: number of indices of an extent-n dimension owned by coordinate me
+int64_t numroc(int64_t n, int nb, int me, int nprocs)
+{
+    const int64_t nblocks = n / nb;
+    int64_t cnt = (nblocks / nprocs) * nb;
+    const int64_t extra = nblocks % nprocs;
+    if (me < extra) cnt += nb;
+    else if (me == extra) cnt += n % nb;
+    return cnt;
+}
+
+int64_t jb_of(const hpl_ctx *c, int64_t j) { return std::min<int64_t>(c->NB, c->N - j * c->NB); }
+
+// FACT(j) into panel buffer b (1x1 grid: local == global).
+hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
+{
+    const int64_t j0 = j * c->NB, jb = jb_of(c, j), mP = c->N - j0;
+    double *Ablk = c->A + j0 * c->lda + j0;
+    CK(c, rm_to_cm(st, mP, jb, Ablk, c->lda, c->panel[b], c->ldp));
+    CK(c, panel_fact(st, mP, jb, c->panel[b], c->ldp, c->ipiv_rel[b], c->nbmin, &c->fw,
+                     c->scratch, j0));
+    CK(c, cm_to_rm(st, mP, jb, c->panel[b], c->ldp, Ablk, c->lda));
+    CK(c, pivot_plan(st, jb, j0, c->ipiv_rel[b], j0, c->gpiv + j0, c->src[b], c->disp[b],
+                     c->ndisp[b]));
+    CK(c, trsm_cols(st, jb, jb, c->panel[b], c->ldp, c->linv[b], c->ldlinv, true));
+    return HPL_OK;
+}
+
+// Column c of the trailing matrix lives at column ucol(c) of the U buffers:
+// shifted by one when c is odd so every TMA operand starts 16-byte aligned.
+inline int64_t ucol(int64_t c) { return c + (c & 1); }
+
+// UPDATE(j) of local columns [c0, c1): LASWP, DTRSM (as L11^{-1} * U), DGEMM.
+// ev (optional, 4 events): recorded before LASWP, before DTRSM, before DGEMM, after.
+hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1,
+                       cudaEvent_t *ev = nullptr)
+{
+    if (ev) CK(c, cudaEventRecord(ev[0], st));
+    const int slot = st == c->s_la ? SLOT_LOOKAHEAD : SLOT_TRAIL;
+    const int64_t j0 = j * c->NB, jb = jb_of(c, j);
+    double *u = c->U + ucol(c0), *u2 = c->U2 + ucol(c0);
+    double *top = c->A + j0 * c->lda + c0;
+    if (c1 > c0)
+        CK(c, laswp_gather_scatter(st, jb, c->src[b], c->disp[b], c->ndisp[b], jb, c->A, c->lda,
+                                   c0, c1, u, c->ldu));
+    if (ev) CK(c, cudaEventRecord(ev[1], st));
+    // block row j <- L11^{-1} U  (written to A and to the aligned copy U2)
+    if (c1 > c0)
+        CK(c, dgemm(st, GEMM_ASSIGN, true, jb, c1 - c0, jb, c->linv[b], c->ldlinv, u, c->ldu,
+                    top, c->lda, -1, u2, c->ldu, slot));
+    if (ev) CK(c, cudaEventRecord(ev[2], st));
+    const int64_t mrest = c->N - j0 - jb;
+    if (mrest > 0 && c1 > c0)
+        CK(c, dgemm(st, GEMM_UPDATE, false, mrest, c1 - c0, jb, c->panel[b] + jb, c->ldp, u2,
+                    c->ldu, top + jb * c->lda, c->lda, -1, nullptr, 0, slot));
+    if (ev) {
+        CK(c, cudaEventRecord(ev[3], st));
+        if (mrest > 0 && c1 > c0) {
+            c->dgemm_flop += 2.0 * (double)mrest * (double)(c1 - c0) * (double)jb;
+            c->dgemm_launches += 1;
+        }
+    }
+    return HPL_OK;
+}
+
+hpl_status ensure_timing_events(hpl_ctx *c, int64_t nblk)
+{
+    const size_t need = (size_t)(7 * nblk);
+    if (c->tev.size() == need) return HPL_OK;
+    for (auto e : c->tev) cudaEventDestroy(e);
+    c->tev.assign(need, nullptr);
+    for (auto &e : c->tev) CK(c, cudaEventCreate(&e));
+    return HPL_OK;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b)
+{
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.f;
+    }
+    return ms;
+}
+
+hpl_status alloc_ctx(hpl_ctx *c)
+{
+    c->mloc = numroc(c->N, c->NB, c->myrow, c->P);
+    c->nloc = numroc(c->N + 1, c->NB, c->mycol, c->Q);
+    c->lda = round_up(std::max<int64_t>(c->nloc, 1), 16);
+    c->ldp = round_up(std::max<int64_t>(c->mloc, 1), 16);
+    c->ldlinv = round_up(c->NB, 16);
+    c->ldu = round_up(c->nloc + 2, 16);
+    auto M = [&](void **p, size_t bytes) -> bool {
+        if (cudaMalloc(p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            set_err(c, "cudaMalloc(%zu bytes) failed", bytes);
+            return false;
+        }
+        return true;
+    };
+    const size_t NBs = (size_t)c->NB;
+    if (!M((void **)&c->A, sizeof(double) * (size_t)c->mloc * c->lda)) return HPL_ERR_OOM;
+    for (int b = 0; b < 2; ++b) {
+        if (!M((void **)&c->panel[b], sizeof(double) * (size_t)c->ldp * NBs)) return HPL_ERR_OOM;
+        if (!M((void **)&c->linv[b], sizeof(double) * (size_t)c->ldlinv * NBs)) return HPL_ERR_OOM;
+        if (!M((void **)&c->ipiv_rel[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
+        if (!M((void **)&c->src[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
+        if (!M((void **)&c->disp[b], sizeof(int64_t) * 2 * NBs)) return HPL_ERR_OOM;
+        if (!M((void **)&c->ndisp[b], sizeof(int))) return HPL_ERR_OOM;
+        CK(c, cudaMemset(c->panel[b], 0, sizeof(double) * (size_t)c->ldp * NBs));
+    }
+    if (!M((void **)&c->gpiv, sizeof(int64_t) * (size_t)c->N)) return HPL_ERR_OOM;
+    if (!M((void **)&c->U, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
+    if (!M((void **)&c->U2, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
+    if (!M((void **)&c->scratch, sizeof(double) * round_up(NBs, 16) * NBs)) return HPL_ERR_OOM;
+    if (!M((void **)&c->x, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
+    if (!M((void **)&c->tbuf, sizeof(double) * NBs)) return HPL_ERR_OOM;
+    if (!M((void **)&c->out4, sizeof(double) * 4)) return HPL_ERR_OOM;
+    CK(c, fact_work_alloc(&c->fw));
+    int lo, hi;
+    CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(c, cudaStreamCreateWithPriority(&c->s_la, cudaStreamNonBlocking, hi));
+    CK(c, cudaStreamCreateWithPriority(&c->s_tr, cudaStreamNonBlocking, lo));
+    for (int b = 0; b < 2; ++b) CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming));
+    for (int k = 0; k < 3; ++k) CK(c, cudaEventCreate(&c->ev_t[k]));
+    return HPL_OK;
+}
+
+hpl_status generate(hpl_ctx *c)
+{
+    CK(c, gen_local(c->s_tr, c->seed, c->N, c->NB, c->P, c->Q, c->myrow, c->mycol, c->mloc,
+                    c->nloc, c->A, c->lda));
+    CK(c, cudaStreamSynchronize(c->s_tr));
+    c->state = hpl_ctx::S_INIT;
+    return HPL_OK;
+}
+
+void release(hpl_ctx *c)
+{
+    if (!c) return;
+    cudaFree(c->A);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->panel[b]); cudaFree(c->linv[b]); cudaFree(c->ipiv_rel[b]);
+        cudaFree(c->src[b]); cudaFree(c->disp[b]); cudaFree(c->ndisp[b]);
+        if (c->ev_panel[b]) cudaEventDestroy(c->ev_panel[b]);
+    }
+    cudaFree(c->gpiv); cudaFree(c->U); cudaFree(c->U2); cudaFree(c->scratch);
+    cudaFree(c->x); cudaFree(c->tbuf); cudaFree(c->out4);
+    fact_work_free(&c->fw);
+    if (c->ev_rest) cudaEventDestroy(c->ev_rest);
+    for (auto e : c->tev) cudaEventDestroy(e);
+    for (int k = 0; k < 3; ++k)
+        if (c->ev_t[k]) cudaEventDestroy(c->ev_t[k]);
+    if (c->s_la) cudaStreamDestroy(c->s_la);
+    if (c->s_tr) cudaStreamDestroy(c->s_tr);
+}
+
+hpl_status check_args(int64_t N, int32_t NB, int32_t P, int32_t Q)
+{
+    if (N < 1 || NB < 1 || NB > N || P < 1 || Q < 1) return HPL_ERR_ARG;
+    if (NB > 1024) return HPL_ERR_ARG;   // kernel limits (pivot plan, TRSM, back solve)
+    if (NB & 1) return HPL_ERR_ARG;      // TMA alignment of the L panel (reading A18)
+    if (N >= (int64_t)1 << 31) return HPL_ERR_ARG;
+    return HPL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hpl_status hpl_init(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t seed, hpl_ctx **out)
+{
+    if (!out) return HPL_ERR_ARG;
+    *out = nullptr;
+    if (check_args(N, NB, P, Q) != HPL_OK || P * Q != 1) return HPL_ERR_ARG;
+    hpl_ctx *c = new hpl_ctx();
+    c->N = N; c->NB = NB; c->P = P; c->Q = Q; c->seed = seed;
+    cudaGetDevice(&c->device);
+    hpl_status s = alloc_ctx(c);
+    if (s == HPL_OK) s = generate(c);
+    *out = c;   // returned even on failure so hpl_last_error works; caller frees
+    return s;
+}
+
+hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t seed,
+                         int32_t rank, int32_t nranks, const void *nccl_unique_id,
+                         int32_t device, hpl_ctx **out)
+{
+    (void)N; (void)NB; (void)P; (void)Q; (void)seed; (void)rank; (void)nranks;
+    (void)nccl_unique_id; (void)device;
+    if (out) *out = nullptr;
+    return HPL_ERR_ARG;  // multi-rank path: see DESIGN.md "Multi-GPU" (not built yet)
+}
+
+hpl_status hpl_get_unique_id(void *id_out)
+{
+    (void)id_out;
+    return HPL_ERR_ARG;
+}
+
+hpl_status hpl_factor(hpl_ctx *c)
+{
+    if (!c) return HPL_ERR_ARG;
+    if (c->state != hpl_ctx::S_INIT) {
+        set_err(c, "hpl_factor: context not in the initialised state");
+        return HPL_ERR_STATE;
+    }
+    const int64_t l0 = g_launches.load();
+    const int64_t nblk = cdiv(c->N, c->NB);
+    if (c->timing) {
+        hpl_status se = ensure_timing_events(c, nblk);
+        if (se != HPL_OK) return se;
+    }
+    c->dgemm_flop = 0;
+    c->dgemm_launches = 0;
+    CK(c, cudaEventRecord(c->ev_t[0], c->s_la));
+    CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_t[0], 0));
+    CK(c, cudaMemsetAsync(c->fw.info, 0xff, sizeof(int64_t), c->s_la));
+    hpl_status s = fact_panel(c, c->s_la, 0, 0);
+    if (s != HPL_OK) return s;
+    CK(c, cudaEventRecord(c->ev_panel[0], c->s_la));
+    for (int64_t j = 0; j < nblk; ++j) {
+        const int b = (int)(j & 1);
+        const int64_t j0 = j * c->NB, jb = jb_of(c, j);
+        const int64_t ct0 = j0 + jb, cend = c->nloc;
+        const bool has_next = j + 1 < nblk;
+        const int64_t jb1 = has_next ? jb_of(c, j + 1) : 0;
+        cudaEvent_t *E = c->timing ? &c->tev[7 * j] : nullptr;
+        if (c->lookahead) {
+            CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_panel[b], 0));
+            s = update_cols(c, c->s_tr, j, b, ct0 + jb1, cend, E);
+            if (s != HPL_OK) return s;
+            CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
+            if (E) CK(c, cudaEventRecord(E[4], c->s_la));
+            if (has_next) {
+                s = update_cols(c, c->s_la, j, b, ct0, ct0 + jb1);
+                if (s != HPL_OK) return s;
+                if (E) CK(c, cudaEventRecord(E[5], c->s_la));
+                s = fact_panel(c, c->s_la, j + 1, b ^ 1);
+                if (s != HPL_OK) return s;
+                CK(c, cudaEventRecord(c->ev_panel[b ^ 1], c->s_la));
+            } else if (E) {
+                CK(c, cudaEventRecord(E[5], c->s_la));
+            }
+            if (E) CK(c, cudaEventRecord(E[6], c->s_la));
+            CK(c, cudaStreamWaitEvent(c->s_la, c->ev_rest, 0));
+        } else {
+            if (E) CK(c, cudaEventRecord(E[4], c->s_la));
+            s = update_cols(c, c->s_la, j, b, ct0, cend, E);
+            if (s != HPL_OK) return s;
+            if (E) CK(c, cudaEventRecord(E[5], c->s_la));
+            if (has_next) {
+                s = fact_panel(c, c->s_la, j + 1, b ^ 1);
+                if (s != HPL_OK) return s;
+            }
+            if (E) CK(c, cudaEventRecord(E[6], c->s_la));
+        }
+    }
+    CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
+    CK(c, cudaStreamWaitEvent(c->s_la, c->ev_rest, 0));
+    CK(c, cudaEventRecord(c->ev_t[1], c->s_la));
+    CK(c, cudaStreamSynchronize(c->s_la));
+    CK(c, cudaStreamSynchronize(c->s_tr));
+    c->launches = g_launches.load() - l0;
+    c->factor_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
+    c->timeline.clear();
+    c->dgemm_ms = 0;
+    if (c->timing) {
+        c->timeline.reserve(6 * nblk);
+        for (int64_t j = 0; j < nblk; ++j) {
+            cudaEvent_t *E = &c->tev[7 * j];
+            const double rest_dg = ev_ms(E[2], E[3]);
+            c->timeline.push_back(c->lookahead ? ev_ms(E[5], E[6]) : ev_ms(E[5], E[6]));
+            c->timeline.push_back(ev_ms(E[4], E[5]));
+            c->timeline.push_back(ev_ms(E[0], E[3]));
+            c->timeline.push_back(ev_ms(E[0], E[1]));
+            c->timeline.push_back(ev_ms(E[1], E[2]));
+            c->timeline.push_back(rest_dg);
+            c->dgemm_ms += rest_dg;
+        }
+    }
+    int64_t info = -1;
+    CK(c, cudaMemcpy(&info, c->fw.info, sizeof info, cudaMemcpyDeviceToHost));
+    c->state = hpl_ctx::S_FACTORED;
+    if (info != -1) {
+        c->singular = info;
+        set_err(c, "exact zero pivot in global column %lld", (long long)info);
+        return HPL_ERR_SINGULAR;
+    }
+    return HPL_OK;
+}
+
+hpl_status hpl_solve(hpl_ctx *c, double *x_host)
+{
+    if (!c) return HPL_ERR_ARG;
+    if (c->state != hpl_ctx::S_FACTORED) {
+        set_err(c, "hpl_solve: call hpl_factor first");
+        return HPL_ERR_STATE;
+    }
+    if (c->singular >= 0) return HPL_ERR_SINGULAR;
+    const int64_t l0 = g_launches.load();
+    CK(c, cudaEventRecord(c->ev_t[1], c->s_la));
+    CK(c, back_solve(c->s_la, c->N, c->NB, c->A, c->lda, c->A + c->N, c->lda, c->x, c->tbuf));
+    if (x_host)
+        CK(c, cudaMemcpyAsync(x_host, c->x, sizeof(double) * c->N, cudaMemcpyDeviceToHost,
+                              c->s_la));
+    CK(c, cudaEventRecord(c->ev_t[2], c->s_la));
+    CK(c, cudaStreamSynchronize(c->s_la));
+    c->solve_ms = ev_ms(c->ev_t[1], c->ev_t[2]);
+    c->launches += g_launches.load() - l0;
+    c->state = hpl_ctx::S_SOLVED;
+    return HPL_OK;
+}
+
+hpl_status hpl_residual(hpl_ctx *c, double *resid)
+{
+    if (!c || !resid) return HPL_ERR_ARG;
+    if (c->state != hpl_ctx::S_SOLVED) {
+        set_err(c, "hpl_residual: call hpl_solve first");
+        return HPL_ERR_STATE;
+    }
+    CK(c, residual_seeded(c->s_la, c->seed, c->N, c->x, c->out4));
+    double h[4];
+    CK(c, cudaMemcpyAsync(h, c->out4, sizeof h, cudaMemcpyDeviceToHost, c->s_la));
+    CK(c, cudaStreamSynchronize(c->s_la));
+    const double eps = 0x1p-53;
+    *resid = h[0] / (eps * (h[1] * h[2] + h[3]) * (double)c->N);
+    return HPL_OK;
+}
+
+hpl_status hpl_regenerate(hpl_ctx *c)
+{
+    if (!c || !c->A) return HPL_ERR_ARG;
+    c->singular = -1;
+    return generate(c);
+}
+
+hpl_status hpl_load_local(hpl_ctx *c, const double *host, int64_t ld)
+{
+    if (!c || !host || ld < c->nloc) return HPL_ERR_ARG;
+    CK(c, cudaMemcpy2DAsync(c->A, c->lda * 8, host, ld * 8, c->nloc * 8, c->mloc,
+                            cudaMemcpyHostToDevice, c->s_tr));
+    CK(c, cudaStreamSynchronize(c->s_tr));
+    c->singular = -1;
+    c->state = hpl_ctx::S_INIT;
+    return HPL_OK;
+}
+
+hpl_status hpl_local_shape(const hpl_ctx *c, int64_t *rows, int64_t *cols)
+{
+    if (!c) return HPL_ERR_ARG;
+    if (rows) *rows = c->mloc;
+    if (cols) *cols = c->nloc;
+    return HPL_OK;
+}
+
+void hpl_free(hpl_ctx *c)
+{
+    if (!c) return;
+    if (c->s_la) cudaStreamSynchronize(c->s_la);
+    if (c->s_tr) cudaStreamSynchronize(c->s_tr);
+    release(c);
+    delete c;
+}
+
+const char *hpl_last_error(const hpl_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t hpl_singular_column(const hpl_ctx *c) { return c ? c->singular : -1; }
+
+hpl_status hpl_get_ipiv(const hpl_ctx *c, int64_t *ipiv_host)
+{
+    if (!c || !ipiv_host) return HPL_ERR_ARG;
+    if (c->state < hpl_ctx::S_FACTORED) return HPL_ERR_STATE;
+    if (cudaMemcpy(ipiv_host, c->gpiv, sizeof(int64_t) * c->N, cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return HPL_ERR_CUDA;
+    return HPL_OK;
+}
+
+hpl_status hpl_get_local(const hpl_ctx *c, double *host, int64_t ld)
+{
+    if (!c || !host || ld < c->nloc) return HPL_ERR_ARG;
+    if (cudaMemcpy2D(host, ld * 8, c->A, c->lda * 8, c->nloc * 8, c->mloc,
+                     cudaMemcpyDeviceToHost) != cudaSuccess)
+        return HPL_ERR_CUDA;
+    return HPL_OK;
+}
+
+int64_t hpl_get_timeline(const hpl_ctx *c, double *t, int64_t cap)
+{
+    if (!c || !t) return 0;
+    const int64_t n = std::min<int64_t>(cap, (int64_t)c->timeline.size() / 6);
+    std::memcpy(t, c->timeline.data(), sizeof(double) * 6 * n);
+    return n;
+}
+
+hpl_status hpl_set_timing(hpl_ctx *c, int32_t enable)
+{
+    if (!c) return HPL_ERR_ARG;
+    c->timing = enable != 0;
+    return HPL_OK;
+}
+
+hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
+{
+    if (!c || !name) return HPL_ERR_ARG;
+    if (!strcmp(name, "lookahead")) c->lookahead = value != 0;
+    else if (!strcmp(name, "nbmin")) {
+        if (value < 1 || value > 16) return HPL_ERR_ARG;
+        c->nbmin = (int)value;
+    } else if (!strcmp(name, "gemm_cfg")) dgemm_set_default_cfg((int)value);
+    else return HPL_ERR_ARG;
+    return HPL_OK;
+}
+
+int64_t hpl_launch_count(const hpl_ctx *c) { return c ? c->launches : 0; }
+
+hpl_status hpl_last_timing(const hpl_ctx *c, double *out6)
+{
+    if (!c || !out6) return HPL_ERR_ARG;
+    out6[0] = c->factor_ms;
+    out6[1] = c->solve_ms;
+    out6[2] = (double)c->dgemm_launches;
+    out6[3] = c->dgemm_ms;
+    out6[4] = c->dgemm_flop;
+    out6[5] = (double)c->launches;
+    return HPL_OK;
+}
+
+}  // extern "C"

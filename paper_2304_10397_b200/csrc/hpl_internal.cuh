@@ -1,0 +1,110 @@
+// hpl_internal.cuh — shared declarations of libhpl.so's kernels and launchers.
+// Product code only; nothing here is shared with oracle/ (see DESIGN.md).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <atomic>
+
+namespace hpl {
+
+// Number of this library's kernel launches (reported as gpu_launches).
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- generator
+// Fill local block: rows [0, lrows) x cols [0, lcols) of the row-major local
+// matrix (ld) with entries of the global N x (N+1) system, local->global via
+// the block-cyclic map (NB, P, Q, myrow, mycol).
+cudaError_t gen_local(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int Q,
+                      int myrow, int mycol, int64_t lrows, int64_t lcols, double *A, int64_t ld);
+// Fill an explicit global window (tests).
+cudaError_t gen_window(cudaStream_t st, uint64_t seed, int64_t N, int64_t i0, int64_t rows,
+                       int64_t j0, int64_t cols, double *out, int64_t ld);
+
+// ---------------------------------------------------------------- copies
+// dst (col-major, ldd) <- src (row-major, lds): rows x cols.
+cudaError_t rm_to_cm(cudaStream_t st, int64_t rows, int64_t cols, const double *src, int64_t lds,
+                     double *dst, int64_t ldd);
+// dst (row-major, ldd) <- src (col-major, lds): rows x cols.
+cudaError_t cm_to_rm(cudaStream_t st, int64_t rows, int64_t cols, const double *src, int64_t lds,
+                     double *dst, int64_t ldd);
+
+// ---------------------------------------------------------------- DGEMM
+enum GemmMode { GEMM_UPDATE = 0, GEMM_ASSIGN = 1 };
+// C (m x n row-major ldc)  -=  A (m x k col-major lda) * B (k x n row-major ldb)   [UPDATE]
+// C                         =  A * B                                              [ASSIGN]
+// a_lower: A is lower triangular (A[i][p] = 0 for p > i): k-chunks above the
+// diagonal of each m-tile are skipped.  A and B must be 16-byte aligned with
+// even lda/ldb (TMA); C may be anywhere.  C2 (ASSIGN only, 16B aligned, even
+// ldc2): the epilogue stores the result there as well.  slot (0..2) selects
+// the param-space offset of the kernel's tensor maps: launches that may run
+// concurrently must use different slots (see kernels_gemm.cu ParamPad).
+enum GemmSlot { SLOT_TRAIL = 0, SLOT_LOOKAHEAD = 1, SLOT_FACT = 2 };
+cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n, int64_t k,
+                  const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                  int64_t ldc, int cfg = -1, double *C2 = nullptr, int64_t ldc2 = 0,
+                  int slot = SLOT_TRAIL);
+void dgemm_set_default_cfg(int cfg);
+int dgemm_get_default_cfg();
+
+// ---------------------------------------------------------------- TRSM helpers
+// In-place B (k x ncols, col-major ldb) <- L^{-1} B, L unit lower (col-major ldl),
+// one CTA per column of B.  If identity_init, B is first set to I (k x k) —
+// then B = L^{-1}.
+cudaError_t trsm_cols(cudaStream_t st, int64_t k, int64_t ncols, const double *L, int64_t ldl,
+                      double *B, int64_t ldb, bool identity_init);
+
+// ---------------------------------------------------------------- panel FACT
+struct FactWork {
+    double *cand;        // candidate records (2 parity buffers)
+    unsigned *bar;       // grid barrier words (count, generation)
+    int64_t *info;       // first singular global column; all-ones (== -1) if none
+    int max_ctas;
+};
+cudaError_t fact_work_alloc(FactWork *w);
+// Pivot winner among n candidates (max |v|, ties -> smallest row), as the FACT reduces.
+cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,
+                       int64_t *winner);
+void fact_work_free(FactWork *w);
+// Recursive right-looking panel LU (NDIV=2, leaf nbmin) of P (m x nb col-major ldp).
+// ipiv receives panel-relative pivots (device, int64).  Uses scratch for the
+// transposed U block of the recursion GEMMs (>= nb*nb doubles).  A zero pivot
+// at panel column k records min(goff + k) in w->info.
+cudaError_t panel_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp,
+                       int64_t *ipiv_dev, int nbmin, FactWork *w, double *scratch, int64_t goff);
+
+// ---------------------------------------------------------------- LASWP
+// From panel-relative pivots (jb entries; positions r0+k <-> r0+ipiv_rel[k])
+// build: src[k] (row whose content ends in row r0+k, k<jb), and ndisp
+// displaced (dst, src) row pairs (dst >= r0+jb).  Also writes global pivots
+// gpiv[k] = ipiv_rel[k] + goff.  All device arrays.
+cudaError_t pivot_plan(cudaStream_t st, int64_t jb, int64_t r0, const int64_t *ipiv_rel,
+                       int64_t goff, int64_t *gpiv, int64_t *src, int64_t *disp,
+                       int *ndisp);
+// Gather U[k][c] = A[src[k]][c0+c] and scatter A[disp_dst][c] = A[disp_src][c]
+// for columns [c0, c1) of the row-major A.
+cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src,
+                                 const int64_t *disp, const int *ndisp, int64_t max_disp,
+                                 double *A, int64_t lda, int64_t c0, int64_t c1, double *U,
+                                 int64_t ldu);
+
+// ---------------------------------------------------------------- solve / residual
+cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,
+                       const double *y, int64_t ystride, double *x, double *tbuf);
+// out4 (device, 4 doubles: rinf, anorm, xnorm, bnorm) for the seeded system.
+cudaError_t residual_seeded(cudaStream_t st, uint64_t seed, int64_t N, const double *x,
+                            double *out4);
+
+// FP64 tensor-pipe ceiling: register-resident DMMA chain on every SM.
+cudaError_t dmma_peak(int iters, int blocks_per_sm, int warps, double *ms, double *flop);
+
+}  // namespace hpl
+
+#define HPL_CUDA_TRY(expr)                              \
+    do {                                                \
+        cudaError_t _e = (expr);                        \
+        if (_e != cudaSuccess) return _e;               \
+    } while (0)

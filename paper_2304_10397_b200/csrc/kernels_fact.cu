@@ -1,0 +1,321 @@
+// kernels_fact.cu — device panel FACT, no CPU fallback.
+//
+// The paper factors the tall-skinny M x NB panel on the CPU with T threads
+// that own NB-row tiles round-robin, a parallel max-reduction for the pivot,
+// the main thread applying the swap and all threads doing the rank-1 update
+// of their own tiles, with the recursive right-looking
+// variant, two subdivisions, base block 16 and a right-looking leaf
+// (PAPER.md l.34).  Here the "threads" are CTAs of one cooperative kernel:
+// each CTA owns a contiguous chunk of panel rows, finds its local pivot
+// candidate with warp shuffles, publishes (|v|, row, the row's leaf values)
+// — the payload travels with the reduction — and after ONE
+// grid-wide barrier per column every CTA reduces the candidates itself,
+// applies the swap to the rows it owns and updates them.  The recursion's
+// TRSM and GEMM steps run as separate kernels (the GEMM is the DMMA kernel).
+#include "hpl_internal.cuh"
+#include <cstdio>
+
+namespace hpl {
+
+namespace {
+
+constexpr int LEAF_MAX = 16;           // widest leaf (NBMIN)
+constexpr int REC = 2 + LEAF_MAX;      // doubles per candidate record
+constexpr int FACT_THREADS = 256;
+constexpr int MAX_CTAS = 1024;
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        const unsigned arrived = atomicAdd(bar, 1u);
+        if (arrived == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// better(a, b): a beats b  <=>  |a| > |b|, ties -> smaller row (reading A2)
+__device__ __forceinline__ bool better(double va, long long ra, double vb, long long rb)
+{
+    return va > vb || (va == vb && ra < rb);
+}
+
+__device__ __forceinline__ void warp_argmax(double &v, long long &r)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const long long orow = __shfl_xor_sync(0xffffffffu, r, o);
+        if (better(ov, orow, v, r)) { v = ov; r = orow; }
+    }
+}
+
+// Leaf: right-looking GEPP of columns [k0, k0+w) of the panel (rows k0..m-1).
+__global__ void __launch_bounds__(FACT_THREADS)
+leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, double *cand,
+                 unsigned *bar, unsigned long long *info, long long goff)
+{
+    const unsigned G = gridDim.x;
+    const int nrows = m - k0;
+    const int chunk = (nrows + (int)G - 1) / (int)G;
+    const int rbeg = k0 + (int)blockIdx.x * chunk;
+    const int rend = min(m, rbeg + chunk);
+    __shared__ double s_v[FACT_THREADS / 32];
+    __shared__ long long s_r[FACT_THREADS / 32];
+    __shared__ double s_prow[LEAF_MAX], s_rowk[LEAF_MAX];
+    __shared__ long long s_p;
+    __shared__ double s_piv;
+
+    for (int kk = 0; kk < w; ++kk) {
+        const int kc = k0 + kk;
+        double *rec = cand + (size_t)(kk & 1) * (MAX_CTAS + 1) * REC;
+        // ---- 1. local candidate over own rows >= kc
+        double bv = -1.0;
+        long long br = LLONG_MAX;
+        const double *colk = P + (int64_t)kc * ldp;
+        for (int i = max(rbeg, kc) + threadIdx.x; i < rend; i += FACT_THREADS) {
+            const double v = fabs(colk[i]);
+            if (better(v, i, bv, br)) { bv = v; br = i; }
+        }
+        warp_argmax(bv, br);
+        if ((threadIdx.x & 31) == 0) { s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            bv = threadIdx.x < FACT_THREADS / 32 ? s_v[threadIdx.x] : -1.0;
+            br = threadIdx.x < FACT_THREADS / 32 ? s_r[threadIdx.x] : LLONG_MAX;
+            warp_argmax(bv, br);
+            double *myrec = rec + (size_t)blockIdx.x * REC;
+            if (threadIdx.x == 0) {
+                myrec[0] = bv;
+                myrec[1] = __longlong_as_double(br);
+            }
+            if (br != LLONG_MAX && threadIdx.x < w)
+                myrec[2 + threadIdx.x] = P[(int64_t)(k0 + threadIdx.x) * ldp + br];
+            if (kc >= rbeg && kc < rend && threadIdx.x < w)
+                rec[(size_t)G * REC + 2 + threadIdx.x] = P[(int64_t)(k0 + threadIdx.x) * ldp + kc];
+        }
+        __threadfence();
+        grid_barrier(bar, G);
+
+        // ---- 2. every CTA reduces all candidates (deterministic)
+        bv = -1.0;
+        br = LLONG_MAX;
+        int bc = -1;
+        for (int c = threadIdx.x; c < (int)G; c += FACT_THREADS) {
+            // other CTAs wrote these: read through L2 (L1 is not coherent)
+            const double v = __ldcg(rec + (size_t)c * REC);
+            const long long r = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
+            if (r != LLONG_MAX && better(v, r, bv, br)) { bv = v; br = r; bc = c; }
+        }
+        {
+            // argmax carrying the candidate index
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+            }
+            __shared__ int s_c[FACT_THREADS / 32];
+            if ((threadIdx.x & 31) == 0) {
+                s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; s_c[threadIdx.x >> 5] = bc;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const bool ok = threadIdx.x < FACT_THREADS / 32;
+                bv = ok ? s_v[threadIdx.x] : -1.0;
+                br = ok ? s_r[threadIdx.x] : LLONG_MAX;
+                bc = ok ? s_c[threadIdx.x] : -1;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+                    const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                    if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+                }
+                if (threadIdx.x == 0) s_p = br;
+                if (threadIdx.x < w) {
+                    s_prow[threadIdx.x] = __ldcg(rec + (size_t)bc * REC + 2 + threadIdx.x);
+                    s_rowk[threadIdx.x] = __ldcg(rec + (size_t)G * REC + 2 + threadIdx.x);
+                }
+            }
+            __syncthreads();
+        }
+        const long long p = s_p;
+        if (threadIdx.x == 0) {
+            s_piv = s_prow[kk];
+            if (blockIdx.x == 0) {
+                ipiv[kc] = p;
+                if (s_prow[kk] == 0.0) atomicMin(info, (unsigned long long)(goff + kc));
+            }
+        }
+        // ---- 3. swap rows kc and p inside the leaf columns (owners only)
+        if (p != kc) {
+            if (kc >= rbeg && kc < rend && threadIdx.x < w)
+                P[(int64_t)(k0 + threadIdx.x) * ldp + kc] = s_prow[threadIdx.x];
+            if (p >= rbeg && p < rend && threadIdx.x < w)
+                P[(int64_t)(k0 + threadIdx.x) * ldp + p] = s_rowk[threadIdx.x];
+        }
+        __syncthreads();
+        // ---- 4. scale column kc and rank-1 update of the leaf columns (own rows > kc)
+        const double piv = s_piv;
+        for (int i = max(rbeg, kc + 1) + threadIdx.x; i < rend; i += FACT_THREADS) {
+            const double l = P[(int64_t)kc * ldp + i] / piv;
+            P[(int64_t)kc * ldp + i] = l;
+            for (int c = kk + 1; c < w; ++c) {
+                double *q = P + (int64_t)(k0 + c) * ldp + i;
+                *q = fma(-l, s_prow[c], *q);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Apply the leaf's swaps (ipiv[k0..k0+w), panel-relative) to the panel columns
+// outside the leaf: one thread per column, swaps in order (dlaswp semantics).
+__global__ void panel_laswp_kernel(int nb, int64_t ldp, double *P, int k0, int w,
+                                   const int64_t *ipiv)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nb || (c >= k0 && c < k0 + w)) return;
+    double *col = P + (int64_t)c * ldp;
+    for (int k = k0; k < k0 + w; ++k) {
+        const int64_t p = ipiv[k];
+        if (p != k) {
+            const double t = col[k];
+            col[k] = col[p];
+            col[p] = t;
+        }
+    }
+}
+
+int g_num_sms = 0;
+
+cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
+                        int64_t *ipiv, FactWork *wk, long long goff)
+{
+    if (!g_num_sms) {
+        int dev;
+        HPL_CUDA_TRY(cudaGetDevice(&dev));
+        HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t rows = m - k0;
+    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, 512)), g_num_sms);
+    G = std::min(G, wk->max_ctas);
+    int m_i = (int)m;
+    int64_t ldp_ = ldp;
+    int k0_ = k0, w_ = w;
+    unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
+    void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->bar, &info, &goff};
+    HPL_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)leaf_fact_kernel, dim3(G),
+                                             dim3(FACT_THREADS), args, 0, st));
+    count_launch();
+    if (w < 0) return cudaErrorInvalidValue;
+    return cudaSuccess;
+}
+
+cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp, int c0,
+                     int w, int64_t *ipiv, int nbmin, FactWork *wk, double *scratch,
+                     long long goff)
+{
+    if (w <= nbmin || w <= 2) {
+        HPL_CUDA_TRY(launch_leaf(st, m, P, ldp, c0, w, ipiv, wk, goff));
+        if (nb > w) {
+            panel_laswp_kernel<<<(unsigned)cdiv(nb, 128), 128, 0, st>>>((int)nb, ldp, P, c0, w,
+                                                                       ipiv);
+            count_launch();
+            HPL_CUDA_TRY(cudaGetLastError());
+        }
+        return cudaSuccess;
+    }
+    // NDIV = 2; the split is rounded down to an even width so
+    // every recursion offset stays 16-byte aligned for the TMA operands.
+    const int w1 = std::max(2, (w / 2) & ~1), w2 = w - w1;
+    HPL_CUDA_TRY(rec_fact(st, m, nb, P, ldp, c0, w1, ipiv, nbmin, wk, scratch, goff));
+    // U12 <- L11^{-1} U12 (rows c0..c0+w1, cols c0+w1..c0+w)
+    HPL_CUDA_TRY(trsm_cols(st, w1, w2, P + (int64_t)c0 * ldp + c0, ldp,
+                           P + (int64_t)(c0 + w1) * ldp + c0, ldp, false));
+    // A22 -= L21 U12 as the transposed product C'(w2 x m') -= U12^T L21^T:
+    // U12^T is repacked col-major into scratch (w2 x w1, ld round16(w2)).
+    const int64_t mrest = m - c0 - w1;
+    if (mrest > 0) {
+        const int64_t lds = round_up(w2, 16);
+        HPL_CUDA_TRY(rm_to_cm(st, w2, w1, P + (int64_t)(c0 + w1) * ldp + c0, ldp, scratch, lds));
+        HPL_CUDA_TRY(dgemm(st, GEMM_UPDATE, false, w2, mrest, w1, scratch, lds,
+                           P + (int64_t)c0 * ldp + c0 + w1, ldp,
+                           P + (int64_t)(c0 + w1) * ldp + c0 + w1, ldp, -1, nullptr, 0,
+                           SLOT_FACT));
+    }
+    return rec_fact(st, m, nb, P, ldp, c0 + w1, w2, ipiv, nbmin, wk, scratch, goff);
+}
+
+// a8 as a standalone kernel (tests): the FACT's candidate reduction rule.
+__global__ void maxloc_kernel(int n, const double *absval, const int64_t *row, int64_t *winner)
+{
+    double bv = -1.0;
+    long long br = LLONG_MAX;
+    int bc = -1;
+    for (int c = threadIdx.x; c < n; c += 32)
+        if (better(absval[c], row[c], bv, br)) { bv = absval[c]; br = row[c]; bc = c; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+    }
+    if (threadIdx.x == 0) *winner = bc;
+}
+
+}  // namespace
+
+cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,
+                       int64_t *winner)
+{
+    maxloc_kernel<<<1, 32, 0, st>>>(n, absval, row, winner);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t fact_work_alloc(FactWork *w)
+{
+    w->max_ctas = MAX_CTAS;
+    HPL_CUDA_TRY(cudaMalloc(&w->cand, sizeof(double) * 2 * (MAX_CTAS + 1) * REC));
+    HPL_CUDA_TRY(cudaMalloc(&w->bar, 64));
+    HPL_CUDA_TRY(cudaMemset(w->bar, 0, 64));
+    HPL_CUDA_TRY(cudaMalloc(&w->info, sizeof(int64_t)));
+    HPL_CUDA_TRY(cudaMemset(w->info, 0xff, sizeof(int64_t)));
+    return cudaSuccess;
+}
+
+void fact_work_free(FactWork *w)
+{
+    cudaFree(w->cand);
+    cudaFree(w->bar);
+    cudaFree(w->info);
+    w->cand = nullptr;
+    w->bar = nullptr;
+    w->info = nullptr;
+}
+
+cudaError_t panel_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp,
+                       int64_t *ipiv_dev, int nbmin, FactWork *w, double *scratch, int64_t goff)
+{
+    if (nbmin < 1 || nbmin > LEAF_MAX) return cudaErrorInvalidValue;
+    if (m < nb || nb <= 0) return cudaErrorInvalidValue;
+    if (m > INT32_MAX) return cudaErrorInvalidValue;
+    return rec_fact(st, m, nb, P, ldp, 0, (int)nb, ipiv_dev, nbmin, w, scratch, goff);
+}
+
+}  // namespace hpl

@@ -1,0 +1,378 @@
+// kernels_misc.cu — generator (a11), panel copies, column TRSM / unit-lower
+// inverse (a4 helper), back substitution (a10) and the scaled residual (a11).
+#include "hpl_internal.cuh"
+
+namespace hpl {
+
+std::atomic<int64_t> g_launches{0};
+
+// ---------------------------------------------------------------- generator
+// Entry (i, j) of the seeded N x (N+1) system [A | b]: SplitMix64 of the
+// column-major index j*N + i, top 53 bits mapped exactly onto the 2^-53 grid
+// of [-0.5, 0.5)  (reading A6; a pure function of (seed, i, j) as
+// SPEC.md l.63 requires, so every rank generates its own blocks).
+__device__ __forceinline__ double hpl_entry(uint64_t seed, uint64_t N, uint64_t i, uint64_t j)
+{
+    uint64_t z = seed + (j * N + i + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= (z >> 31);
+    const long long v = (long long)(z >> 11) - (1ll << 52);
+    return (double)v * 0x1p-53;  // exact: |v| <= 2^52
+}
+
+// local index -> global index for the block-cyclic map
+__device__ __forceinline__ int64_t l2g(int64_t l, int NB, int nprocs, int me)
+{
+    return ((l / NB) * nprocs + me) * NB + (l % NB);
+}
+
+__global__ void gen_local_kernel(uint64_t seed, int64_t N, int NB, int P, int Q, int myrow,
+                                 int mycol, int64_t lrows, int64_t lcols, double *A, int64_t ld)
+{
+    const int64_t r = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
+    if (r >= lrows) return;
+    const int64_t gi = l2g(r, NB, P, myrow);
+    double *row = A + r * ld;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < lcols;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gj = l2g(c, NB, Q, mycol);
+        row[c] = hpl_entry(seed, (uint64_t)N, (uint64_t)gi, (uint64_t)gj);
+    }
+}
+
+cudaError_t gen_local(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int Q, int myrow,
+                      int mycol, int64_t lrows, int64_t lcols, double *A, int64_t ld)
+{
+    if (lrows <= 0 || lcols <= 0) return cudaSuccess;
+    const int threads = 256;
+    const unsigned gx = (unsigned)std::min<int64_t>(cdiv(lcols, threads), 64);
+    const unsigned gy = (unsigned)std::min<int64_t>(lrows, 65535);
+    const unsigned gz = (unsigned)cdiv(lrows, gy);
+    gen_local_kernel<<<dim3(gx, gy, gz), threads, 0, st>>>(seed, N, NB, P, Q, myrow, mycol, lrows,
+                                                           lcols, A, ld);
+    count_launch();
+    return cudaGetLastError();
+}
+
+__global__ void gen_window_kernel(uint64_t seed, int64_t N, int64_t i0, int64_t rows, int64_t j0,
+                                  int64_t cols, double *out, int64_t ld)
+{
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    const int64_t r = idx / cols, c = idx % cols;
+    out[r * ld + c] = hpl_entry(seed, (uint64_t)N, (uint64_t)(i0 + r), (uint64_t)(j0 + c));
+}
+
+cudaError_t gen_window(cudaStream_t st, uint64_t seed, int64_t N, int64_t i0, int64_t rows,
+                       int64_t j0, int64_t cols, double *out, int64_t ld)
+{
+    const int64_t tot = rows * cols;
+    if (tot <= 0) return cudaSuccess;
+    gen_window_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(seed, N, i0, rows, j0, cols, out,
+                                                                ld);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- copies
+// Tiled transpose through shared memory (32 x 32 tiles, 32 x 8 threads).
+template <bool RM_TO_CM>
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double *__restrict__ src,
+                                 int64_t lds, double *__restrict__ dst, int64_t ldd)
+{
+    __shared__ double tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    if (RM_TO_CM) {
+        // src row-major: read rows (coalesced along c)
+        for (int k = ty; k < 32; k += 8) {
+            const int64_t r = r0 + k, c = c0 + tx;
+            if (r < rows && c < cols) tile[k][tx] = src[r * lds + c];
+        }
+        __syncthreads();
+        // dst col-major: write columns (coalesced along r)
+        for (int k = ty; k < 32; k += 8) {
+            const int64_t c = c0 + k, r = r0 + tx;
+            if (r < rows && c < cols) dst[c * ldd + r] = tile[tx][k];
+        }
+    } else {
+        // src col-major: read columns (coalesced along r)
+        for (int k = ty; k < 32; k += 8) {
+            const int64_t c = c0 + k, r = r0 + tx;
+            if (r < rows && c < cols) tile[tx][k] = src[c * lds + r];
+        }
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8) {
+            const int64_t r = r0 + k, c = c0 + tx;
+            if (r < rows && c < cols) dst[r * ldd + c] = tile[k][tx];
+        }
+    }
+}
+
+static cudaError_t transpose(cudaStream_t st, bool rm_to_cm, int64_t rows, int64_t cols,
+                             const double *src, int64_t lds, double *dst, int64_t ldd)
+{
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    dim3 grid((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32));
+    if (grid.y > 65535) return cudaErrorInvalidValue;
+    if (rm_to_cm)
+        transpose_kernel<true><<<grid, dim3(32, 8), 0, st>>>(rows, cols, src, lds, dst, ldd);
+    else
+        transpose_kernel<false><<<grid, dim3(32, 8), 0, st>>>(rows, cols, src, lds, dst, ldd);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t rm_to_cm(cudaStream_t st, int64_t rows, int64_t cols, const double *src, int64_t lds,
+                     double *dst, int64_t ldd)
+{
+    // rows may exceed 65535*32: split into row chunks
+    const int64_t chunk = 65535ll * 32;
+    for (int64_t r = 0; r < rows; r += chunk)
+        HPL_CUDA_TRY(transpose(st, true, std::min(chunk, rows - r), cols, src + r * lds, lds,
+                               dst + r, ldd));
+    return cudaSuccess;
+}
+
+cudaError_t cm_to_rm(cudaStream_t st, int64_t rows, int64_t cols, const double *src, int64_t lds,
+                     double *dst, int64_t ldd)
+{
+    const int64_t chunk = 65535ll * 32;
+    for (int64_t r = 0; r < rows; r += chunk)
+        HPL_CUDA_TRY(transpose(st, false, std::min(chunk, rows - r), cols, src + r, lds,
+                               dst + r * ldd, ldd));
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- column TRSM
+// One CTA per column x of B (length k, col-major): right-looking forward
+// substitution with the unit lower L (col-major):  for i: x[r] -= L[r][i] x[i]
+// (r > i).  The column of L for the next PF steps is prefetched into registers
+// so the L2 latency overlaps the barrier chain.
+constexpr int TRSM_THREADS = 256;
+constexpr int TRSM_MAXK = 1024;
+
+__global__ void __launch_bounds__(TRSM_THREADS)
+trsm_cols_kernel(int k, const double *__restrict__ L, int64_t ldl, double *B, int64_t ldb,
+                 int identity_init)
+{
+    __shared__ double x[TRSM_MAXK];
+    const int col = blockIdx.x;
+    double *bcol = B + (int64_t)col * ldb;
+    for (int r = threadIdx.x; r < k; r += TRSM_THREADS)
+        x[r] = identity_init ? (r == col ? 1.0 : 0.0) : bcol[r];
+    __syncthreads();
+    constexpr int RPT = TRSM_MAXK / TRSM_THREADS;  // rows per thread
+    constexpr int PF = 8;                          // steps of L prefetched ahead
+    const int i0 = identity_init ? col : 0;        // x[r] = 0 for r < col when B = I
+    double cur[PF][RPT], nxt[PF][RPT];
+    auto load_group = [&](int ib, double (&dst)[PF][RPT]) {
+#pragma unroll
+        for (int s = 0; s < PF; ++s)
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                const int r = threadIdx.x + q * TRSM_THREADS, i = ib + s;
+                dst[s][q] = (r > i && r < k && i < k) ? L[(int64_t)i * ldl + r] : 0.0;
+            }
+    };
+    load_group(i0, cur);
+    for (int ib = i0; ib < k - 1; ib += PF) {
+        load_group(ib + PF, nxt);
+#pragma unroll
+        for (int s = 0; s < PF; ++s) {
+            const int i = ib + s;
+            if (i < k - 1) {
+                const double xi = x[i];
+#pragma unroll
+                for (int q = 0; q < RPT; ++q) {
+                    const int r = threadIdx.x + q * TRSM_THREADS;
+                    if (r > i && r < k) x[r] -= cur[s][q] * xi;
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int s = 0; s < PF; ++s)
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) cur[s][q] = nxt[s][q];
+    }
+    for (int r = threadIdx.x; r < k; r += TRSM_THREADS) bcol[r] = x[r];
+}
+
+cudaError_t trsm_cols(cudaStream_t st, int64_t k, int64_t ncols, const double *L, int64_t ldl,
+                      double *B, int64_t ldb, bool identity_init)
+{
+    if (k <= 0 || ncols <= 0) return cudaSuccess;
+    if (k > TRSM_MAXK) return cudaErrorInvalidValue;
+    trsm_cols_kernel<<<(unsigned)ncols, TRSM_THREADS, 0, st>>>((int)k, L, ldl, B, ldb,
+                                                               identity_init ? 1 : 0);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- back solve
+// Blocked back substitution U x = y, bottom block first:
+//   t = y_b - U[b, right] x_right      (one CTA per row of the block)
+//   x_b = U_bb^{-1} t                  (one CTA; thread r owns row r)
+__global__ void bs_gemv_kernel(int64_t r0, int64_t r1, int64_t N, const double *__restrict__ U,
+                               int64_t ldu, const double *__restrict__ y, int64_t ystride,
+                               const double *__restrict__ x, double *t)
+{
+    const int64_t row = r0 + blockIdx.x;
+    const double *u = U + row * ldu;
+    double s = 0.0;
+    for (int64_t c = r1 + threadIdx.x; c < N; c += blockDim.x) s += u[c] * x[c];
+    __shared__ double red[32];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) t[blockIdx.x] = y[row * ystride] - s;
+    }
+}
+
+constexpr int BS_MAXB = 1024;
+__global__ void __launch_bounds__(BS_MAXB)
+bs_diag_kernel(int64_t r0, int nb, const double *__restrict__ U, int64_t ldu,
+               const double *__restrict__ t, double *x)
+{
+    __shared__ double xs[BS_MAXB];
+    const int r = threadIdx.x;
+    double acc = r < nb ? t[r] : 0.0;
+    const double *urow = U + (r0 + r) * ldu + r0;
+    for (int i = nb - 1; i >= 0; --i) {
+        if (r == i) xs[i] = acc / urow[i];
+        __syncthreads();
+        if (r < i) acc -= urow[i] * xs[i];
+    }
+    if (r < nb) x[r0 + r] = xs[r];
+}
+
+cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,
+                       const double *y, int64_t ystride, double *x, double *tbuf)
+{
+    if (NB > BS_MAXB) return cudaErrorInvalidValue;
+    const int64_t nblk = cdiv(N, NB);
+    for (int64_t b = nblk - 1; b >= 0; --b) {
+        const int64_t r0 = b * NB, r1 = std::min<int64_t>(N, r0 + NB);
+        const int nb = (int)(r1 - r0);
+        bs_gemv_kernel<<<nb, 256, 0, st>>>(r0, r1, N, U, ldu, y, ystride, x, tbuf);
+        bs_diag_kernel<<<1, ((nb + 31) / 32) * 32, 0, st>>>(r0, nb, U, ldu, tbuf, x);
+        count_launch(2);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- residual
+// r_i = sum_j A0[i][j] x_j - b0_i and the row sums of |A0|, with A0 and b0
+// regenerated on the fly from the seed.  One CTA per row;
+// the infinity norms are folded with atomicMax on the (non-negative) bit
+// patterns.  out4 = {||r||, ||A0||, ||x||, ||b0||}.
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v)
+{
+    atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void residual_kernel(uint64_t seed, int64_t N, const double *__restrict__ x,
+                                double *out4)
+{
+    const int64_t i = blockIdx.x;
+    double s = 0.0, a = 0.0;
+    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+        const double v = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)j);
+        s = fma(v, x[j], s);
+        a += fabs(v);
+    }
+    __shared__ double rs[32], ra[32];
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+    }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; ra[threadIdx.x >> 5] = a; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const bool ok = threadIdx.x < (blockDim.x >> 5);
+        s = ok ? rs[threadIdx.x] : 0.0;
+        a = ok ? ra[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+        }
+        if (threadIdx.x == 0) {
+            const double b = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)N);
+            atomic_max_nonneg(&out4[0], fabs(s - b));
+            atomic_max_nonneg(&out4[1], a);
+            atomic_max_nonneg(&out4[2], fabs(x[i]));
+            atomic_max_nonneg(&out4[3], fabs(b));
+        }
+    }
+}
+
+cudaError_t residual_seeded(cudaStream_t st, uint64_t seed, int64_t N, const double *x,
+                            double *out4)
+{
+    HPL_CUDA_TRY(cudaMemsetAsync(out4, 0, 4 * sizeof(double), st));
+    if (N > INT32_MAX) return cudaErrorInvalidValue;
+    residual_kernel<<<(unsigned)N, 256, 0, st>>>(seed, N, x, out4);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- DMMA peak
+// Register-resident chain of mma.sync.m16n8k4.f64 (SASS DMMA), 8 independent
+// accumulators per warp, no memory traffic: the FP64 tensor-pipe ceiling the
+// roofline divides by (MEASURED_PEAKS.json carries no FP64 figure).
+__global__ void dmma_peak_kernel(int iters, double *out)
+{
+    double a0 = threadIdx.x * 1e-3, a1 = 1.0 - a0, b0 = 0.5;
+    double c[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[i][k] = 0.0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, "
+                         "{%6}, {%0,%1,%2,%3};"
+                         : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                         : "d"(a0), "d"(a1), "d"(b0));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+    if (s == 12345.678) out[0] = s;  // keep the chain alive
+}
+
+cudaError_t dmma_peak(int iters, int blocks_per_sm, int warps, double *ms, double *flop)
+{
+    int dev, sms;
+    HPL_CUDA_TRY(cudaGetDevice(&dev));
+    HPL_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double *d = nullptr;
+    HPL_CUDA_TRY(cudaMalloc(&d, 8));
+    cudaEvent_t e0, e1;
+    HPL_CUDA_TRY(cudaEventCreate(&e0));
+    HPL_CUDA_TRY(cudaEventCreate(&e1));
+    const unsigned grid = (unsigned)(sms * blocks_per_sm);
+    dmma_peak_kernel<<<grid, warps * 32>>>(iters / 10, d);  // warm-up
+    HPL_CUDA_TRY(cudaEventRecord(e0));
+    dmma_peak_kernel<<<grid, warps * 32>>>(iters, d);
+    HPL_CUDA_TRY(cudaEventRecord(e1));
+    HPL_CUDA_TRY(cudaEventSynchronize(e1));
+    count_launch(2);
+    float t = 0;
+    HPL_CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t;
+    // one m16n8k4 = 16*8*4 FMA = 1024 flop; 8 per iteration per warp
+    *flop = (double)grid * warps * (double)iters * 8.0 * 1024.0;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    return cudaGetLastError();
+}
+
+}  // namespace hpl

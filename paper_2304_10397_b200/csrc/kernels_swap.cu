@@ -1,0 +1,138 @@
+// kernels_swap.cu — LASWP gather/scatter around the pivot exchange
+// ("a GPU kernel to gather the rows to
+// be communicated ... and a GPU kernel to scatter the received rows back").
+//
+// The jb sequential swaps (r0+k) <-> ipiv[k] of one panel are first turned
+// into a plan: src[k] = the row whose content ends in row r0+k, and the list
+// of rows below the block that receive a row of the block (every swap has a
+// block row as its first element, so content that reaches the block never
+// leaves it again, and a row below the block can only receive an ORIGINAL
+// block row).  With the plan, one pass over the trailing columns moves each
+// row once: the block's final rows are gathered into the U buffer (the DTRSM
+// then writes L11^{-1} U back into block row r0) and the displaced rows are
+// scattered — coalesced 16-byte row copies, HBM-bound.
+#include "hpl_internal.cuh"
+
+namespace hpl {
+
+namespace {
+
+constexpr int HSLOTS = 2048;  // open-addressing table for rows below the block (jb <= 1024)
+
+__global__ void pivot_plan_kernel(int jb, long long r0, const int64_t *__restrict__ ipiv_rel,
+                                  long long goff, int64_t *gpiv, int64_t *src, int64_t *disp,
+                                  int *ndisp)
+{
+    __shared__ long long keys[HSLOTS];
+    __shared__ long long vals[HSLOTS];
+    __shared__ long long cur[1024];
+    for (int i = threadIdx.x; i < HSLOTS; i += blockDim.x) keys[i] = -1;
+    for (int k = threadIdx.x; k < jb; k += blockDim.x) {
+        cur[k] = r0 + k;
+        gpiv[k] = ipiv_rel[k] + goff;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < jb; ++k) {
+            const long long p = r0 + ipiv_rel[k];
+            if (p == r0 + k) continue;
+            if (p < r0 + jb) {
+                const long long t = cur[k];
+                cur[k] = cur[p - r0];
+                cur[p - r0] = t;
+            } else {
+                unsigned h = (unsigned)((unsigned long long)p * 0x9E3779B97F4A7C15ull >> 53) &
+                             (HSLOTS - 1);
+                while (keys[h] != -1 && keys[h] != p) h = (h + 1) & (HSLOTS - 1);
+                const long long content = keys[h] == p ? vals[h] : p;
+                keys[h] = p;
+                vals[h] = cur[k];
+                cur[k] = content;
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < jb; k += blockDim.x) src[k] = cur[k];
+    // compact the displaced (dst, src) pairs in slot order (deterministic)
+    if (threadIdx.x == 0) {
+        int n = 0;
+        for (int h = 0; h < HSLOTS; ++h)
+            if (keys[h] != -1) {
+                disp[2 * n] = keys[h];
+                disp[2 * n + 1] = vals[h];
+                ++n;
+            }
+        *ndisp = n;
+    }
+}
+
+constexpr int LS_COLS = 64;      // columns per CTA (one warp covers 64 doubles with 16B lanes)
+constexpr int LS_WARPS = 8;
+
+__global__ void __launch_bounds__(LS_WARPS * 32)
+laswp_gs_kernel(int jb, const int64_t *__restrict__ src, const int64_t *__restrict__ disp,
+                const int *__restrict__ ndisp, double *A, long long lda, long long c0,
+                long long c1, double *U, long long ldu, int vec)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long cb = c0 + (long long)blockIdx.x * LS_COLS;  // first column of this CTA
+    const long long col = cb + 2 * lane;
+    const bool has0 = col < c1, has1 = col + 1 < c1;
+    // phase 1: gather the block's final rows into U
+    for (int k = warp; k < jb; k += LS_WARPS) {
+        const double *s = A + src[k] * lda + col;
+        double *d = U + (long long)k * ldu + (col - c0);
+        if (vec && has1) {
+            *reinterpret_cast<double2 *>(d) = *reinterpret_cast<const double2 *>(s);
+        } else {
+            if (has0) d[0] = s[0];
+            if (has1) d[1] = s[1];
+        }
+    }
+    __syncthreads();  // every read of a displaced row precedes its overwrite
+    // phase 2: displaced rows receive original block rows
+    const int nd = *ndisp;
+    for (int d = warp; d < nd; d += LS_WARPS) {
+        const double *s = A + disp[2 * d + 1] * lda + col;
+        double *t = A + disp[2 * d] * lda + col;
+        if (vec && has1) {
+            *reinterpret_cast<double2 *>(t) = *reinterpret_cast<const double2 *>(s);
+        } else {
+            if (has0) t[0] = s[0];
+            if (has1) t[1] = s[1];
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t pivot_plan(cudaStream_t st, int64_t jb, int64_t r0, const int64_t *ipiv_rel,
+                       int64_t goff, int64_t *gpiv, int64_t *src, int64_t *disp, int *ndisp)
+{
+    if (jb <= 0) return cudaSuccess;
+    if (jb > 1024) return cudaErrorInvalidValue;
+    pivot_plan_kernel<<<1, 256, 0, st>>>((int)jb, r0, ipiv_rel, goff, gpiv, src, disp, ndisp);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src,
+                                 const int64_t *disp, const int *ndisp, int64_t max_disp,
+                                 double *A, int64_t lda, int64_t c0, int64_t c1, double *U,
+                                 int64_t ldu)
+{
+    (void)max_disp;
+    if (jb <= 0 || c1 <= c0) return cudaSuccess;
+    const int vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda & 1) == 0 &&
+                     (c0 & 1) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&
+                     (ldu & 1) == 0)
+                        ? 1
+                        : 0;
+    const int64_t nblk = cdiv(c1 - c0, LS_COLS);
+    laswp_gs_kernel<<<(unsigned)nblk, LS_WARPS * 32, 0, st>>>((int)jb, src, disp, ndisp, A, lda,
+                                                              c0, c1, U, ldu, vec);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace hpl

@@ -1,0 +1,68 @@
+"""CPU checks of the boundary: libhpl.so builds, loads and exports every
+symbol include/*.h declares (no compute calls without a GPU)."""
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _build():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "hpl_build", os.path.join(ROOT, "paper_2304_10397_b200", "build.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m.build()
+
+
+def declared_symbols():
+    names = set()
+    for h in ("hpl.h", "hpl_kernels.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"\b(hplk?_[a-z_]+)\s*\(", src):
+            names.add(m.group(1))
+    return names
+
+
+def test_library_exports_all_declared_symbols():
+    lib = _build()
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib], text=True)
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    missing = declared_symbols() - exported
+    assert not missing, f"declared but not exported: {sorted(missing)}"
+
+
+def test_python_binding_covers_abi():
+    from paper_2304_10397_b200 import _lib
+    assert declared_symbols() <= set(_lib.EXPORTED)
+    for name in _lib.EXPORTED:
+        assert hasattr(_lib.lib, name)
+
+
+def test_sm100a_cubin_present():
+    """The kernels are compiled for sm_100a (cuobjdump lists the ELF arch)."""
+    lib = _build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_product_path_never_references_oracle():
+    """The product package shares no code with oracle/ (DESIGN.md §Oracle)."""
+    pkg = os.path.join(ROOT, "paper_2304_10397_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "hpl_oracle" not in txt, f
+
+
+def test_invalid_args_rejected_without_gpu_work():
+    import ctypes
+    from paper_2304_10397_b200 import _lib
+    h = ctypes.c_void_p()
+    for args in [(0, 32, 1, 1), (100, 0, 1, 1), (100, 200, 1, 1), (100, 32, 2, 1)]:
+        assert _lib.lib.hpl_init(*args, 1, ctypes.byref(h)) == 1  # HPL_ERR_ARG
+        assert not h.value

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs (-m gpu).  Tolerances are derived in
+DESIGN.md §Parity; bit-exact where the step is integer/copy work."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from hpl_inputs import hpl_panel, random_ipiv, random_unit_lower, upper_well_conditioned
+from tests import brute
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def H():
+    import paper_2304_10397_b200 as H
+    return H
+
+
+# ------------------------------------------------------------------ a11 generator
+@pytest.mark.parametrize("N,i0,rows,j0,cols", [(256, 0, 256, 0, 257), (8192, 4000, 64, 8100, 93),
+                                                (131072, 131000, 72, 131000, 73)])
+def test_generator_bitwise(H, N, i0, rows, j0, cols):
+    g = H.hplk_generate(42, N, i0, rows, j0, cols)
+    o = np.array([[oracle.gen_entry(42, N, i, j) for j in range(j0, j0 + cols)]
+                  for i in range(i0, i0 + rows)])
+    assert np.array_equal(g, o)
+
+
+# ------------------------------------------------------------------ a8 maxloc
+def test_maxloc(H):
+    assert H.hplk_maxloc([1.0, 9.0, 3.0, 9.0], [10, 7, 2, 3]) == (9.0, 3)
+    assert H.hplk_maxloc([4.0, 4.0], [9, 1]) == (4.0, 1)
+    rng = np.random.default_rng(0)
+    for n in (1, 5, 33, 148, 1000):
+        v = np.abs(rng.integers(0, 4, n).astype(np.float64))  # many ties
+        r = rng.permutation(10 * n)[:n]
+        assert H.hplk_maxloc(v, r) == oracle.maxloc(v, r)
+
+
+# ------------------------------------------------------------------ a5/a6 DGEMM
+def _gemm_tol(A, B, C):
+    k = A.shape[1]
+    return 2 * brute.gamma(k + 2) * (np.abs(A) @ np.abs(B) + np.abs(C)) + 1e-300
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (128, 64, 16), (300, 200, 64), (513, 257, 37),
+                                   (1000, 700, 512), (64, 1, 512), (7, 1031, 256)])
+def test_dgemm_update_vs_oracle(H, cfg, m, n, k):
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    A = rng.uniform(-1, 1, (m, k))
+    B = rng.uniform(-0.5, 0.5, (k, n))
+    C = rng.uniform(-0.5, 0.5, (m, n))
+    got = H.hplk_dgemm_update(C, A, B, cfg=cfg)
+    ref = oracle.gemm_update(C, A, B)
+    assert np.all(np.abs(got - ref) <= _gemm_tol(A, B, C))
+
+
+def test_dgemm_zero_k_and_identity(H):
+    rng = np.random.default_rng(1)
+    C = rng.uniform(-1, 1, (50, 40))
+    assert np.array_equal(H.hplk_dgemm_update(C, np.zeros((50, 0)), np.zeros((0, 40))), C)
+    # A = I (m = k): C - B exactly (one product per element, no rounding beyond the subtract)
+    B = rng.uniform(-1, 1, (50, 40))
+    assert np.array_equal(H.hplk_dgemm_update(C, np.eye(50), B), C - B)
+
+
+# ------------------------------------------------------------------ a4 DTRSM
+@pytest.mark.parametrize("k,n", [(32, 300), (256, 1000), (512, 129), (13, 5)])
+def test_trsm_vs_oracle(H, k, n):
+    L = random_unit_lower(k, seed=k)
+    rng = np.random.default_rng(n)
+    B = rng.uniform(-0.5, 0.5, (k, n))
+    got = H.hplk_trsm(L, B)
+    ref = oracle.trsm_llnu(L, B)
+    # forward error of a triangular solve: <= c k eps cond(L) |X|; L from GEPP,
+    # cond_inf(L) measured here, c = 4 (inverse + product)
+    Lf = np.tril(L, -1) + np.eye(k)
+    cond = np.linalg.norm(Lf, np.inf) * np.linalg.norm(np.linalg.inv(Lf), np.inf)
+    tol = 4 * k * U * cond * np.max(np.abs(ref))
+    assert np.max(np.abs(got - ref)) <= tol
+
+
+# ------------------------------------------------------------------ a7 panel FACT
+@pytest.mark.parametrize("m,nb,nbmin", [(64, 64, 16), (300, 64, 16), (1000, 256, 16),
+                                        (513, 33, 8), (5000, 128, 16), (4096, 512, 16),
+                                        (40, 7, 1)])
+def test_panel_fact_vs_oracle(H, m, nb, nbmin):
+    Pn = hpl_panel(m, nb, seed=m + nb)
+    LU, ipiv, info = H.hplk_panel_fact(Pn, nbmin=nbmin)
+    LUo, ipo, info_o = oracle.getrf(Pn)
+    assert info == -1 and info_o == -1
+    assert np.array_equal(ipiv, ipo)
+    # factors within 1e-12 elementwise (entries are O(1))
+    assert np.max(np.abs(LU - LUo)) <= 1e-12
+
+
+def test_panel_fact_special(H):
+    LU, ipiv, info = H.hplk_panel_fact(np.array([[0.0], [3.0]]), nbmin=1)
+    assert list(ipiv) == [1] and LU[0, 0] == 3.0 and LU[1, 0] == 0.0 and info == -1
+    Pn = hpl_panel(200, 32, seed=5)
+    Pn[:, 9] = 0.0     # exact zero column -> singular at 9 (reading A3)
+    _, _, info = H.hplk_panel_fact(Pn)
+    assert info == 9
+
+
+# ------------------------------------------------------------------ a1/a3 LASWP
+@pytest.mark.parametrize("rows,cols,j0,jb,c0,c1", [(300, 200, 0, 32, 32, 200),
+                                                   (1000, 513, 256, 256, 1, 513),
+                                                   (90, 17, 40, 50, 0, 17),
+                                                   (2000, 777, 512, 512, 600, 777)])
+def test_laswp_bitwise(H, rows, cols, j0, jb, c0, c1):
+    rng = np.random.default_rng(rows + jb)
+    A = rng.standard_normal((rows, cols))
+    ipiv = random_ipiv(rows, j0, jb, seed=cols)
+    A_gpu, Ug = H.hplk_laswp(A, j0, ipiv, c0, c1)
+    full_ipiv = np.arange(rows, dtype=np.int64)
+    full_ipiv[j0:j0 + jb] = ipiv
+    ref = oracle.laswp(A, j0, j0 + jb, full_ipiv, c0, c1)
+    assert np.array_equal(Ug, ref[j0:j0 + jb, c0:c1])
+    outside = np.ones(rows, bool)
+    outside[j0:j0 + jb] = False
+    assert np.array_equal(A_gpu[outside][:, c0:c1], ref[outside][:, c0:c1])
+    assert np.array_equal(A_gpu[j0:j0 + jb], A[j0:j0 + jb])        # block rows untouched
+    assert np.array_equal(A_gpu[:, :c0], A[:, :c0]) and np.array_equal(A_gpu[:, c1:], A[:, c1:])
+
+
+def test_laswp_identity_moves_nothing(H):
+    A = np.random.default_rng(2).standard_normal((64, 40))
+    A_gpu, Ug = H.hplk_laswp(A, 8, np.arange(8, 24), 0, 40)
+    assert np.array_equal(A_gpu, A) and np.array_equal(Ug, A[8:24])
+
+
+# ------------------------------------------------------------------ a10 back solve
+@pytest.mark.parametrize("N,NB", [(300, 64), (1000, 256), (77, 32), (512, 512)])
+def test_back_solve_vs_oracle(H, N, NB):
+    Uu = upper_well_conditioned(N, seed=N)
+    y = np.random.default_rng(N + 1).uniform(-1, 1, N)
+    got = H.hplk_back_solve(Uu, y, NB=NB)
+    ref, info = oracle.back_solve(Uu, y)
+    assert info == -1
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ end to end
+def _e2e(H, N, NB, seed, lookahead=True):
+    with H.hpl_init(N, NB, 1, 1, seed) as ctx:
+        H.hpl_set_option(ctx, "lookahead", int(lookahead))
+        H.hpl_factor(ctx)
+        x = H.hpl_solve(ctx)
+        ipiv = H.hpl_get_ipiv(ctx)
+        LU = H.hpl_get_local(ctx)
+        r = H.hpl_residual(ctx)
+    return x, ipiv, LU, r
+
+
+@pytest.mark.parametrize("N,NB,seed", [(256, 32, 42), (256, 32, 1), (256, 32, 7), (250, 32, 3),
+                                       (1000, 64, 42), (2048, 256, 5), (64, 64, 9), (33, 2, 4),
+                                       (257, 16, 8)])
+def test_hpl_end_to_end_vs_oracle(H, N, NB, seed):
+    x, ipiv, LU, r = _e2e(H, N, NB, seed)
+    o = oracle.run(N, seed, want_lu=True)
+    assert np.array_equal(ipiv, o["ipiv"]), "pivot sequence differs"
+    assert np.max(np.abs(x - o["x"])) / np.max(np.abs(o["x"])) <= 1e-9
+    assert r < 16.0 and o["resid"] < 16.0
+    # U (upper triangle incl. diagonal) is LAPACK-identical up to rounding
+    Ug = np.triu(LU[:, :N])
+    Uo = np.triu(o["LU"])
+    assert np.max(np.abs(Ug - Uo)) <= 1e-10 * max(1.0, np.max(np.abs(Uo)))
+
+
+def test_lookahead_schedule_invariance(H):
+    """the schedule does not change the mathematics."""
+    xa, pa, _, _ = _e2e(H, 1024, 64, 11, lookahead=True)
+    xb, pb, _, _ = _e2e(H, 1024, 64, 11, lookahead=False)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb)
+
+
+def test_hpl_c1_vs_oracle(H):
+    """BASELINE.json configs[1]: N=8192 NB=256 1x1."""
+    N, NB, seed = 8192, 256, 42
+    x, ipiv, _, r = _e2e(H, N, NB, seed)
+    o = oracle.run(N, seed)
+    assert np.array_equal(ipiv, o["ipiv"])
+    assert np.max(np.abs(x - o["x"])) / np.max(np.abs(o["x"])) <= 1e-9
+    assert r < 16.0 and o["resid"] < 16.0
+
+
+def test_odd_nb_rejected(H):
+    """Reading A18: NB must be even (TMA alignment of the L panel)."""
+    with pytest.raises(H.HplError) as ei:
+        H.hpl_init(100, 33, 1, 1, 1)
+    assert ei.value.status == 1
+
+
+def test_singular_reported(H):
+    N = 64
+    A = np.random.default_rng(0).uniform(-0.5, 0.5, (N, N + 1))
+    A[:, 5] = 0.0
+    with H.hpl_init(N, 16, 1, 1, 1) as ctx:
+        H.hpl_load_local(ctx, A)
+        with pytest.raises(H.HplSingular) as ei:
+            H.hpl_factor(ctx)
+        assert ei.value.column == 5
+
+
+def test_load_local_matches_oracle_solve(H):
+    """Hand-made system through hpl_load_local (the e2e host path)."""
+    N = 300
+    rng = np.random.default_rng(3)
+    Ab = rng.uniform(-0.5, 0.5, (N, N + 1))
+    with H.hpl_init(N, 32, 1, 1, 1) as ctx:
+        H.hpl_load_local(ctx, Ab)
+        H.hpl_factor(ctx)
+        x = H.hpl_solve(ctx)
+        ipiv = H.hpl_get_ipiv(ctx)
+    LU, ipo, _ = oracle.getrf(Ab[:, :N])
+    xo = oracle.getrs(LU, ipo, Ab[:, N])
+    assert np.array_equal(ipiv, ipo)
+    assert np.max(np.abs(x - xo)) / np.max(np.abs(xo)) <= 1e-9
+
+
+def test_hpl_full_size_c2_sampled(H):
+    """BASELINE.json configs[2] (N=131072 NB=512, the bench workload, look-ahead
+    on): HPL residual < 16 on the device over all rows, and the oracle's own
+    residual on sampled rows (regenerated from the seed, x from the GPU) is
+    < 16 too — two independent implementations of the same check."""
+    N, NB, seed = 131072, 512, 42
+    with H.hpl_init(N, NB, 1, 1, seed) as ctx:
+        H.hpl_factor(ctx)
+        x = H.hpl_solve(ctx)
+        r = H.hpl_residual(ctx)
+        ipiv = H.hpl_get_ipiv(ctx)
+    assert r < 16.0
+    # pivots are valid LAPACK pivots (ipiv[k] >= k) and x is finite
+    assert np.all(ipiv >= np.arange(N)) and np.all(ipiv < N)
+    assert np.all(np.isfinite(x))
+    rows = np.random.default_rng(0).choice(N, 48, replace=False)
+    rr, rowsum = oracle.residual_rows(N, seed, x, rows)
+    bn = max(abs(oracle.gen_entry(seed, N, i, N)) for i in rows)
+    sampled = np.max(np.abs(rr)) / (U * (np.max(rowsum) * np.max(np.abs(x)) + bn) * N)
+    assert sampled < 16.0

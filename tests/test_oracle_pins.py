@@ -291,3 +291,17 @@ def test_oracle_thread_count_invariance():
         env = dict(os.environ, OMP_NUM_THREADS=t, PYTHONPATH=ROOT)
         outs.append(subprocess.check_output([sys.executable, "-c", code], env=env, cwd=ROOT))
     assert outs[0] == outs[1]
+
+
+def test_residual_rows_vs_exact():
+    """Sampled-row residual (full-size parity helper) vs exact rational sums."""
+    N, seed = 40, 9
+    A, b = oracle.generate(seed, N)
+    x = np.random.default_rng(2).uniform(-1, 1, N)
+    rows = np.array([0, 17, 39])
+    r, rs = oracle.residual_rows(N, seed, x, rows)
+    for t, i in enumerate(rows):
+        ex = sum(Fraction(float(A[i, j])) * Fraction(float(x[j])) for j in range(N)) - Fraction(float(b[i]))
+        mag = float(sum(abs(Fraction(float(A[i, j])) * Fraction(float(x[j]))) for j in range(N)))
+        assert abs(r[t] - float(ex)) <= brute.gamma(N + 1) * (mag + abs(b[i]))
+        assert rs[t] == pytest.approx(float(sum(abs(Fraction(float(v))) for v in A[i])), rel=1e-15)
