@@ -1,0 +1,7 @@
+"""Two launches of the trailing-update DGEMM (warm-up + measured) at an HPL
+shape, for `ncu --set full -k regex:dgemm -s 1 -c 1`."""
+import sys
+import paper_2304_10397_b200 as H
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+ms = H.hplk_dgemm_bench(m, m, 512, cfg=-1, reps=1)
+print("ms", ms, "TF", 2 * m * m * 512 / (ms[0] * 1e-3) / 1e12)
