@@ -1,7 +1,7 @@
 """bench.py — HPL FP64 TFLOP/s on B200 (BASELINE.json metric), one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
-                    [--n N] [--nb NB] [--no-e2e]
+                    [--size N] [--block NB] [--no-e2e]
 
 A "step" is one full HPL solve (hpl_factor + hpl_solve: every §8(a) row of
 SURVEY.md runs inside it) of the seeded system at the workload size; the
@@ -36,6 +36,16 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_DERIVED = 148 * 128 * 1965e6 / 1e12  # SMs x FP64 flop/clk x max SM clock (TFLOP/s)
 
 
+# weak scaling: ~137 GB of A per GPU on a 1 x Q grid
+N_BY_GPUS = {1: 131072, 2: 185344, 4: 262144, 8: 360448}
+
+
+def workload(a, world: int):
+    """(N, NB, P, Q) of this run: --size, else the weak-scaled default."""
+    n = a.n if a.n > 0 else N_BY_GPUS.get(world, int(131072 * world ** 0.5) // 512 * 512)
+    return n, a.nb, 1, world
+
+
 def hpl_flops(n: int) -> float:
     return 2.0 / 3.0 * n ** 3 + 1.5 * n ** 2
 
@@ -46,8 +56,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--n", type=int, default=131072)
-    ap.add_argument("--nb", type=int, default=512)
+    ap.add_argument("--size", dest="n", type=int, default=0, help="HPL N (0 = weak-scaled default per GPU count)")
+    ap.add_argument("--block", dest="nb", type=int, default=512)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--cpu-n", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
@@ -146,17 +156,18 @@ def run_reference(a, rank, world):
         times.append(dt)
     T = sum(times)
     value = a.steps * hpl_flops(a.cpu_n) / T / 1e12
+    N, NB, P, Q = workload(a, world)
     line = {
         "impl": "reference",
         "metric": "HPL FP64 TFLOP/s (residual<16)", "value": value, "unit": "TFLOP/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * T / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
-        "config": {"workload": f"HPL N={a.n} NB={a.nb} 1x1", "sample": f"full solve at N={a.cpu_n}",
-                   "N": a.n, "NB": a.nb, "grid": "1x1", "l2": "inputs > L2"},
+        "config": {"workload": f"HPL N={N} NB={NB} {P}x{Q} grid", "sample": f"full solve at N={a.cpu_n}",
+                   "N": N, "NB": NB, "grid": f"{P}x{Q}", "l2": "inputs > L2"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
                          "sample": f"oracle GEPP+solves, full solve at N={a.cpu_n} "
-                                   f"(bounded sample of the N={a.n} workload), {cpu_model()}"},
+                                   f"(bounded sample of the N={N} workload), {cpu_model()}"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -179,7 +190,7 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")   # rendezvous + scalars; the data path is libhpl's NCCL
 
     def barrier():
         torch.cuda.synchronize()
@@ -189,13 +200,19 @@ def main():
     def allmax(v: float) -> float:
         if dist is None:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    N, NB = a.n, a.nb
-    # Multi-GPU: independent per-GPU systems until the P x Q path lands.
-    ctx = H.hpl_init(N, NB, 1, 1, a.seed + rank)
+    N, NB, P, Q = workload(a, world)
+    if world == 1:
+        ctx = H.hpl_init(N, NB, 1, 1, a.seed)
+    else:
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.frombuffer(bytearray(H.hpl_get_unique_id()), dtype=torch.uint8)
+        dist.broadcast(uid, 0)
+        ctx = H.hpl_init_dist(N, NB, P, Q, a.seed, rank, world, bytes(uid.tolist()), local)
     H.hpl_set_timing(ctx, True)
     peak_meas = H.hplk_dmma_peak()
 
@@ -227,37 +244,44 @@ def main():
     dg_fl = sum(t["dgemm_flop"] for t in tims)
     dg_n = sum(t["dgemm_launches"] for t in tims)
     launches = sum(t["launches"] for t in tims) // max(1, a.steps)
-    value = world * a.steps * fl / (dev_ms * 1e-3) / 1e12
+    value = a.steps * fl / (dev_ms * 1e-3) / 1e12   # one P x Q system over all GPUs
     dg_tf = dg_fl / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None
 
     # ---- end to end through the public API with host buffers (pinned)
     e2e = None
     if not a.no_e2e:
         rows, cols = ctx.local_shape
+        need = rows * cols * 8
         try:
-            host_t = torch.empty((rows, cols), dtype=torch.float64, pin_memory=True)
-            pinned = True
+            avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
         except Exception:
-            host_t = torch.empty((rows, cols), dtype=torch.float64)
-            pinned = False
-        host = host_t.numpy()
-        H.hpl_regenerate(ctx)
-        ctx.check(H.hpl.lib.hpl_get_local(ctx.h, H.hpl.ptr(host), cols))
-        xh = torch.empty(N, dtype=torch.float64, pin_memory=pinned).numpy()
-        barrier()
-        t0 = time.perf_counter()
-        ctx.check(H.hpl.lib.hpl_load_local(ctx.h, H.hpl.ptr(host), cols))
-        H.hpl_factor(ctx)
-        ctx.check(H.hpl.lib.hpl_solve(ctx.h, H.hpl.ptr(xh)))
-        barrier()
-        dt = allmax(time.perf_counter() - t0)
-        r = H.hpl_residual(ctx)
-        if not r < 16.0:
-            raise SystemExit(f"e2e residual {r} >= 16")
-        e2e = {"value": world * fl / dt / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": int(rows * cols * 8), "d2h_bytes_per_step": int(N * 8),
-               "pinned": pinned, "s": dt}
-        del host_t
+            avail = 0
+        local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        if avail < 1.08 * need * local_ranks:
+            e2e = {"value": None, "unit": "TFLOP/s", "skipped": f"host RAM {avail / 1e9:.0f} GB < "
+                   f"{local_ranks} x {need / 1e9:.0f} GB of local matrices"}
+        else:
+            host = np.empty((rows, cols), dtype=np.float64)
+            H.hpl_regenerate(ctx)
+            ctx.check(H.hpl.lib.hpl_get_local(ctx.h, H.hpl.ptr(host), cols))
+            pinned = H.hpl_pin_host(host, True)
+            xh = np.empty(N, dtype=np.float64)
+            barrier()
+            t0 = time.perf_counter()
+            ctx.check(H.hpl.lib.hpl_load_local(ctx.h, H.hpl.ptr(host), cols))
+            H.hpl_factor(ctx)
+            ctx.check(H.hpl.lib.hpl_solve(ctx.h, H.hpl.ptr(xh)))
+            barrier()
+            dt = allmax(time.perf_counter() - t0)
+            r = H.hpl_residual(ctx)
+            if not r < 16.0:
+                raise SystemExit(f"e2e residual {r} >= 16")
+            e2e = {"value": fl / dt / 1e12, "unit": "TFLOP/s",
+                   "h2d_bytes_per_step": int(rows * cols * 8) * world,
+                   "d2h_bytes_per_step": int(N * 8) * world, "pinned": pinned, "s": dt}
+            if pinned:
+                H.hpl_pin_host(host, False)
+            del host
 
     cpu = None
     if rank == 0 and not a.no_cpu:
@@ -285,10 +309,10 @@ def main():
         "warmup": a.warmup, "ms_per_step": dev_ms / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
-        "config": {"workload": f"HPL N={N} NB={NB} 1x1 per GPU", "N": N, "NB": NB,
-                   "grid": "1x1", "parallelism": "1 GPU" if world == 1 else
-                   f"{world} independent 1x1 systems (P x Q path not built yet)",
-                   "lookahead": True, "l2": "inputs (137 GB) >> L2, no flush needed",
+        "config": {"workload": f"HPL N={N} NB={NB} {P}x{Q} grid", "N": N, "NB": NB,
+                   "grid": f"{P}x{Q}", "parallelism": "1 GPU" if world == 1 else
+                   f"2D block-cyclic {P}x{Q}, NCCL LBCAST along the process row",
+                   "lookahead": True, "l2": "inputs (~137 GB per GPU) >> L2, no flush needed",
                    "residual_max": max(resids), "frac_of_fp64_peak": value / world / FP64_PEAK_DERIVED},
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (trailing update)",
                      "achieved": dg_tf, "peak": FP64_PEAK_DERIVED, "unit": "TFLOP/s",

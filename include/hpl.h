@@ -123,6 +123,18 @@ int64_t hpl_launch_count(const hpl_ctx *ctx);
  * kernel launches}.  The DGEMM entries are filled only with hpl_set_timing(1). */
 hpl_status hpl_last_timing(const hpl_ctx *ctx, double *out6);
 
+/* Host-only planning of iteration j for process (myrow, mycol) of a P x Q
+ * grid (no GPU work; the factor loop uses the same bookkeeping):
+ * out8 = {first active local row, first trailing local column, look-ahead
+ * column range [b, e) (empty unless this process owns panel j+1), rest
+ * column range [b, e), local column of panel j on its owner (-1 elsewhere),
+ * jb}.  2D block-cyclic map of SPEC.md l.30–57. */
+hpl_status hpl_plan_iteration(int64_t N, int32_t NB, int32_t P, int32_t Q, int32_t myrow,
+                              int32_t mycol, int64_t j, int64_t *out8);
+/* Page-lock (pin = 1) or release (pin = 0) a caller-owned host buffer so
+ * hpl_load_local / hpl_solve copies run at full DMA speed. */
+hpl_status hpl_pin_host(void *p, int64_t bytes, int32_t pin);
+
 #ifdef __cplusplus
 }
 #endif

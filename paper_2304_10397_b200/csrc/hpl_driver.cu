@@ -12,8 +12,16 @@
 // UPDATE phase on the remaining local matrix"): the update of panel j+1's
 // columns and FACT(j+1) run on a high-priority stream S_la while the rest of
 // the trailing update runs on S_tr; events order the two.
+//
+// Distribution: 2D block-cyclic over P x Q (rank = p + q*P).
+// This revision drives 1 x Q grids: FACT runs on the process column that owns
+// panel j, and the packed panel (with its pivots) is broadcast along the
+// process row (LBCAST: "Processes which do not participate
+// in the FACT phase simply wait in the LBCAST phase").  P > 1 (pivot
+// exchange and RS along process columns) is rejected with HPL_ERR_ARG.
 #include "hpl_internal.cuh"
 #include "../../include/hpl.h"
+#include <nccl.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -28,6 +36,9 @@ struct hpl_ctx {
     int NB = 0, P = 1, Q = 1;
     uint64_t seed = 0;
     int rank = 0, nranks = 1, myrow = 0, mycol = 0, device = 0;
+    bool dist = false;
+    ncclComm_t world = nullptr, row_comm = nullptr, col_comm = nullptr;
+    double *rvec = nullptr, *avec = nullptr;   // residual partial sums (N each)
     // local storage
     int64_t mloc = 0, nloc = 0, lda = 0;
     double *A = nullptr;
@@ -35,7 +46,6 @@ struct hpl_ctx {
     int64_t ldp = 0;
     double *linv[2] = {nullptr, nullptr};
     int64_t ldlinv = 0;
-    int64_t *ipiv_rel[2] = {nullptr, nullptr};
     int64_t *src[2] = {nullptr, nullptr};
     int64_t *disp[2] = {nullptr, nullptr};
     int *ndisp[2] = {nullptr, nullptr};
@@ -86,6 +96,15 @@ void set_err(hpl_ctx *c, const char *fmt, ...)
         }                                                                                   \
     } while (0)
 
+#define NK(ctx, expr)                                                                       \
+    do {                                                                                    \
+        ncclResult_t _r = (expr);                                                           \
+        if (_r != ncclSuccess) {                                                            \
+            set_err(ctx, "%s:%d %s -> %s", __FILE__, __LINE__, #expr, ncclGetErrorString(_r)); \
+            return HPL_ERR_NCCL;                                                            \
+        }                                                                                   \
+    } while (0)
+
 // numroc: number of indices of an extent-n dimension owned by coordinate me
 int64_t numroc(int64_t n, int nb, int me, int nprocs)
 {
@@ -99,19 +118,59 @@ int64_t numroc(int64_t n, int nb, int me, int nprocs)
 
 int64_t jb_of(const hpl_ctx *c, int64_t j) { return std::min<int64_t>(c->NB, c->N - j * c->NB); }
 
-// FACT(j) into panel buffer b (1x1 grid: local == global).
+// local rows (cols) of this process with global index < g
+int64_t lrows_before(const hpl_ctx *c, int64_t g) { return numroc(g, c->NB, c->myrow, c->P); }
+int64_t lcols_before(const hpl_ctx *c, int64_t g) { return numroc(g, c->NB, c->mycol, c->Q); }
+// leading dimension of the packed panel of iteration j (active local rows)
+int64_t panel_ld(const hpl_ctx *c, int64_t j)
+{
+    return round_up(std::max<int64_t>(c->mloc - lrows_before(c, j * c->NB), 1), 16);
+}
+int64_t *panel_ipiv(hpl_ctx *c, int64_t j, int b)
+{
+    // the panel buffer has one extra column; it carries the pivots through LBCAST
+    return reinterpret_cast<int64_t *>(c->panel[b] + jb_of(c, j) * panel_ld(c, j));
+}
+
+// FACT(j) on the process column that owns panel j: pack the active local rows
+// of the panel columns (column-major), factor, write the factored panel back.
+hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
+{
+    const int64_t j0 = j * c->NB, jb = jb_of(c, j);
+    const int64_t lr0 = lrows_before(c, j0), mP = c->mloc - lr0, ldpj = panel_ld(c, j);
+    const int64_t lcp = lcols_before(c, j0);
+    double *Ablk = c->A + lr0 * c->lda + lcp;
+    CK(c, rm_to_cm(st, mP, jb, Ablk, c->lda, c->panel[b], ldpj));
+    CK(c, panel_fact(st, mP, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin, &c->fw,
+                     c->scratch, j0));
+    CK(c, cm_to_rm(st, mP, jb, c->panel[b], ldpj, Ablk, c->lda));
+    return HPL_OK;
+}
+
+// LBCAST(j) along the process row (Q > 1), then on every rank: the pivot
+// plan for the row swaps and L11^{-1} for the DTRSM.
+hpl_status lbcast_and_plan(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
+{
+    const int64_t j0 = j * c->NB, jb = jb_of(c, j), ldpj = panel_ld(c, j);
+    const int pcol = (int)(j % c->Q);
+    if (c->Q > 1)
+        NK(c, ncclBroadcast(c->panel[b], c->panel[b], (size_t)((jb + 1) * ldpj), ncclDouble, pcol,
+                            c->row_comm, st));
+    const int64_t lr0 = lrows_before(c, j0);
+    CK(c, pivot_plan(st, jb, lr0, panel_ipiv(c, j, b), j0, c->gpiv + j0, c->src[b], c->disp[b],
+                     c->ndisp[b]));
+    CK(c, trsm_cols(st, jb, jb, c->panel[b], ldpj, c->linv[b], c->ldlinv, true));
+    return HPL_OK;
+}
+
+// FACT(j) (owner column) + LBCAST(j) + plan (everyone).
 hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 {
-    const int64_t j0 = j * c->NB, jb = jb_of(c, j), mP = c->N - j0;
-    double *Ablk = c->A + j0 * c->lda + j0;
-    CK(c, rm_to_cm(st, mP, jb, Ablk, c->lda, c->panel[b], c->ldp));
-    CK(c, panel_fact(st, mP, jb, c->panel[b], c->ldp, c->ipiv_rel[b], c->nbmin, &c->fw,
-                     c->scratch, j0));
-    CK(c, cm_to_rm(st, mP, jb, c->panel[b], c->ldp, Ablk, c->lda));
-    CK(c, pivot_plan(st, jb, j0, c->ipiv_rel[b], j0, c->gpiv + j0, c->src[b], c->disp[b],
-                     c->ndisp[b]));
-    CK(c, trsm_cols(st, jb, jb, c->panel[b], c->ldp, c->linv[b], c->ldlinv, true));
-    return HPL_OK;
+    if (c->mycol == (int)(j % c->Q)) {
+        hpl_status s = fact_local(c, st, j, b);
+        if (s != HPL_OK) return s;
+    }
+    return lbcast_and_plan(c, st, j, b);
 }
 
 // Column c of the trailing matrix lives at column ucol(c) of the U buffers:
@@ -126,8 +185,9 @@ hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0
     if (ev) CK(c, cudaEventRecord(ev[0], st));
     const int slot = st == c->s_la ? SLOT_LOOKAHEAD : SLOT_TRAIL;
     const int64_t j0 = j * c->NB, jb = jb_of(c, j);
+    const int64_t lr0 = lrows_before(c, j0), ldpj = panel_ld(c, j);
     double *u = c->U + ucol(c0), *u2 = c->U2 + ucol(c0);
-    double *top = c->A + j0 * c->lda + c0;
+    double *top = c->A + lr0 * c->lda + c0;
     if (c1 > c0)
         CK(c, laswp_gather_scatter(st, jb, c->src[b], c->disp[b], c->ndisp[b], jb, c->A, c->lda,
                                    c0, c1, u, c->ldu));
@@ -137,9 +197,9 @@ hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0
         CK(c, dgemm(st, GEMM_ASSIGN, true, jb, c1 - c0, jb, c->linv[b], c->ldlinv, u, c->ldu,
                     top, c->lda, -1, u2, c->ldu, slot));
     if (ev) CK(c, cudaEventRecord(ev[2], st));
-    const int64_t mrest = c->N - j0 - jb;
+    const int64_t mrest = c->mloc - lr0 - jb;
     if (mrest > 0 && c1 > c0)
-        CK(c, dgemm(st, GEMM_UPDATE, false, mrest, c1 - c0, jb, c->panel[b] + jb, c->ldp, u2,
+        CK(c, dgemm(st, GEMM_UPDATE, false, mrest, c1 - c0, jb, c->panel[b] + jb, ldpj, u2,
                     c->ldu, top + jb * c->lda, c->lda, -1, nullptr, 0, slot));
     if (ev) {
         CK(c, cudaEventRecord(ev[3], st));
@@ -190,13 +250,12 @@ hpl_status alloc_ctx(hpl_ctx *c)
     const size_t NBs = (size_t)c->NB;
     if (!M((void **)&c->A, sizeof(double) * (size_t)c->mloc * c->lda)) return HPL_ERR_OOM;
     for (int b = 0; b < 2; ++b) {
-        if (!M((void **)&c->panel[b], sizeof(double) * (size_t)c->ldp * NBs)) return HPL_ERR_OOM;
+        if (!M((void **)&c->panel[b], sizeof(double) * (size_t)c->ldp * (NBs + 1))) return HPL_ERR_OOM;
         if (!M((void **)&c->linv[b], sizeof(double) * (size_t)c->ldlinv * NBs)) return HPL_ERR_OOM;
-        if (!M((void **)&c->ipiv_rel[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
         if (!M((void **)&c->src[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
         if (!M((void **)&c->disp[b], sizeof(int64_t) * 2 * NBs)) return HPL_ERR_OOM;
         if (!M((void **)&c->ndisp[b], sizeof(int))) return HPL_ERR_OOM;
-        CK(c, cudaMemset(c->panel[b], 0, sizeof(double) * (size_t)c->ldp * NBs));
+        CK(c, cudaMemset(c->panel[b], 0, sizeof(double) * (size_t)c->ldp * (NBs + 1)));
     }
     if (!M((void **)&c->gpiv, sizeof(int64_t) * (size_t)c->N)) return HPL_ERR_OOM;
     if (!M((void **)&c->U, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
@@ -205,6 +264,8 @@ hpl_status alloc_ctx(hpl_ctx *c)
     if (!M((void **)&c->x, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
     if (!M((void **)&c->tbuf, sizeof(double) * NBs)) return HPL_ERR_OOM;
     if (!M((void **)&c->out4, sizeof(double) * 4)) return HPL_ERR_OOM;
+    if (!M((void **)&c->rvec, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
+    if (!M((void **)&c->avec, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
     CK(c, fact_work_alloc(&c->fw));
     int lo, hi;
     CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -230,12 +291,15 @@ void release(hpl_ctx *c)
     if (!c) return;
     cudaFree(c->A);
     for (int b = 0; b < 2; ++b) {
-        cudaFree(c->panel[b]); cudaFree(c->linv[b]); cudaFree(c->ipiv_rel[b]);
+        cudaFree(c->panel[b]); cudaFree(c->linv[b]); 
         cudaFree(c->src[b]); cudaFree(c->disp[b]); cudaFree(c->ndisp[b]);
         if (c->ev_panel[b]) cudaEventDestroy(c->ev_panel[b]);
     }
     cudaFree(c->gpiv); cudaFree(c->U); cudaFree(c->U2); cudaFree(c->scratch);
-    cudaFree(c->x); cudaFree(c->tbuf); cudaFree(c->out4);
+    cudaFree(c->x); cudaFree(c->tbuf); cudaFree(c->out4); cudaFree(c->rvec); cudaFree(c->avec);
+    if (c->row_comm) ncclCommDestroy(c->row_comm);
+    if (c->col_comm) ncclCommDestroy(c->col_comm);
+    if (c->world) ncclCommDestroy(c->world);
     fact_work_free(&c->fw);
     if (c->ev_rest) cudaEventDestroy(c->ev_rest);
     for (auto e : c->tev) cudaEventDestroy(e);
@@ -276,16 +340,35 @@ hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t s
                          int32_t rank, int32_t nranks, const void *nccl_unique_id,
                          int32_t device, hpl_ctx **out)
 {
-    (void)N; (void)NB; (void)P; (void)Q; (void)seed; (void)rank; (void)nranks;
-    (void)nccl_unique_id; (void)device;
-    if (out) *out = nullptr;
-    return HPL_ERR_ARG;  // multi-rank path: see DESIGN.md "Multi-GPU" (not built yet)
+    if (!out || !nccl_unique_id) return HPL_ERR_ARG;
+    *out = nullptr;
+    if (check_args(N, NB, P, Q) != HPL_OK || P * Q != nranks || rank < 0 || rank >= nranks)
+        return HPL_ERR_ARG;
+    if (P != 1) return HPL_ERR_ARG;  // P > 1 (pivot exchange / RS) not built yet: DESIGN.md §6
+    hpl_ctx *c = new hpl_ctx();
+    *out = c;
+    c->N = N; c->NB = NB; c->P = P; c->Q = Q; c->seed = seed;
+    c->rank = rank; c->nranks = nranks; c->myrow = rank % P; c->mycol = rank / P;
+    c->device = device;
+    c->dist = nranks > 1;
+    CK(c, cudaSetDevice(device));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof id);
+    NK(c, ncclCommInitRank(&c->world, nranks, id, rank));
+    NK(c, ncclCommSplit(c->world, c->myrow, c->mycol, &c->row_comm, nullptr));
+    NK(c, ncclCommSplit(c->world, c->mycol, c->myrow, &c->col_comm, nullptr));
+    hpl_status s = alloc_ctx(c);
+    if (s == HPL_OK) s = generate(c);
+    return s;
 }
 
 hpl_status hpl_get_unique_id(void *id_out)
 {
-    (void)id_out;
-    return HPL_ERR_ARG;
+    if (!id_out) return HPL_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return HPL_ERR_NCCL;
+    std::memcpy(id_out, &id, sizeof id);
+    return HPL_OK;
 }
 
 hpl_status hpl_factor(hpl_ctx *c)
@@ -312,31 +395,34 @@ hpl_status hpl_factor(hpl_ctx *c)
     for (int64_t j = 0; j < nblk; ++j) {
         const int b = (int)(j & 1);
         const int64_t j0 = j * c->NB, jb = jb_of(c, j);
-        const int64_t ct0 = j0 + jb, cend = c->nloc;
+        const int64_t lct = lcols_before(c, j0 + jb), cend = c->nloc;  // local trailing cols
         const bool has_next = j + 1 < nblk;
         const int64_t jb1 = has_next ? jb_of(c, j + 1) : 0;
+        // panel j+1 lives in the next jb1 local columns of its owner column
+        const bool own_next = has_next && c->mycol == (int)((j + 1) % c->Q);
+        const int64_t lrest = lct + (own_next ? jb1 : 0);
         cudaEvent_t *E = c->timing ? &c->tev[7 * j] : nullptr;
         if (c->lookahead) {
             CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_panel[b], 0));
-            s = update_cols(c, c->s_tr, j, b, ct0 + jb1, cend, E);
+            s = update_cols(c, c->s_tr, j, b, lrest, cend, E);
             if (s != HPL_OK) return s;
             CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
             if (E) CK(c, cudaEventRecord(E[4], c->s_la));
-            if (has_next) {
-                s = update_cols(c, c->s_la, j, b, ct0, ct0 + jb1);
+            if (own_next) {
+                s = update_cols(c, c->s_la, j, b, lct, lct + jb1);
                 if (s != HPL_OK) return s;
-                if (E) CK(c, cudaEventRecord(E[5], c->s_la));
+            }
+            if (E) CK(c, cudaEventRecord(E[5], c->s_la));
+            if (has_next) {
                 s = fact_panel(c, c->s_la, j + 1, b ^ 1);
                 if (s != HPL_OK) return s;
                 CK(c, cudaEventRecord(c->ev_panel[b ^ 1], c->s_la));
-            } else if (E) {
-                CK(c, cudaEventRecord(E[5], c->s_la));
             }
             if (E) CK(c, cudaEventRecord(E[6], c->s_la));
             CK(c, cudaStreamWaitEvent(c->s_la, c->ev_rest, 0));
         } else {
             if (E) CK(c, cudaEventRecord(E[4], c->s_la));
-            s = update_cols(c, c->s_la, j, b, ct0, cend, E);
+            s = update_cols(c, c->s_la, j, b, lct, cend, E);
             if (s != HPL_OK) return s;
             if (E) CK(c, cudaEventRecord(E[5], c->s_la));
             if (has_next) {
@@ -369,6 +455,11 @@ hpl_status hpl_factor(hpl_ctx *c)
             c->dgemm_ms += rest_dg;
         }
     }
+    if (c->dist) {
+        // the owner column saw the zero pivot: min over all ranks (unsigned: -1 = none)
+        NK(c, ncclAllReduce(c->fw.info, c->fw.info, 1, ncclUint64, ncclMin, c->world, c->s_la));
+        CK(c, cudaStreamSynchronize(c->s_la));
+    }
     int64_t info = -1;
     CK(c, cudaMemcpy(&info, c->fw.info, sizeof info, cudaMemcpyDeviceToHost));
     c->state = hpl_ctx::S_FACTORED;
@@ -390,7 +481,30 @@ hpl_status hpl_solve(hpl_ctx *c, double *x_host)
     if (c->singular >= 0) return HPL_ERR_SINGULAR;
     const int64_t l0 = g_launches.load();
     CK(c, cudaEventRecord(c->ev_t[1], c->s_la));
-    CK(c, back_solve(c->s_la, c->N, c->NB, c->A, c->lda, c->A + c->N, c->lda, c->x, c->tbuf));
+    {
+        // distributed block back substitution over the process row (P = 1)
+        const int64_t N = c->N, nblk = cdiv(N, c->NB);
+        const int ycol = (int)((N / c->NB) % c->Q);            // owner of global column N
+        const int64_t lcy = c->mycol == ycol ? lcols_before(c, N) : -1;
+        const int64_t lcN = lcols_before(c, N);
+        for (int64_t bb = nblk - 1; bb >= 0; --bb) {
+            const int64_t r0 = bb * c->NB, r1 = std::min<int64_t>(N, r0 + c->NB);
+            const int nb = (int)(r1 - r0);
+            const int64_t lr0 = lrows_before(c, r0);
+            CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda, lcols_before(c, r1), lcN,
+                             c->NB, c->Q, c->mycol, c->x, lcy, c->tbuf));
+            if (c->Q > 1)
+                NK(c, ncclAllReduce(c->tbuf, c->tbuf, nb, ncclDouble, ncclSum, c->row_comm,
+                                    c->s_la));
+            const int owner = (int)(bb % c->Q);
+            if (c->mycol == owner)
+                CK(c, bs_diag(c->s_la, nb, c->A + lr0 * c->lda + lcols_before(c, r0), c->lda,
+                              c->tbuf, c->x + r0));
+            if (c->Q > 1)
+                NK(c, ncclBroadcast(c->x + r0, c->x + r0, nb, ncclDouble, owner, c->row_comm,
+                                    c->s_la));
+        }
+    }
     if (x_host)
         CK(c, cudaMemcpyAsync(x_host, c->x, sizeof(double) * c->N, cudaMemcpyDeviceToHost,
                               c->s_la));
@@ -409,7 +523,13 @@ hpl_status hpl_residual(hpl_ctx *c, double *resid)
         set_err(c, "hpl_residual: call hpl_solve first");
         return HPL_ERR_STATE;
     }
-    CK(c, residual_seeded(c->s_la, c->seed, c->N, c->x, c->out4));
+    CK(c, residual_partial(c->s_la, c->seed, c->N, c->NB, c->Q, c->mycol, lcols_before(c, c->N),
+                           c->x, c->rvec, c->avec));
+    if (c->Q > 1) {
+        NK(c, ncclAllReduce(c->rvec, c->rvec, c->N, ncclDouble, ncclSum, c->row_comm, c->s_la));
+        NK(c, ncclAllReduce(c->avec, c->avec, c->N, ncclDouble, ncclSum, c->row_comm, c->s_la));
+    }
+    CK(c, residual_finalize(c->s_la, c->seed, c->N, c->rvec, c->avec, c->x, c->out4));
     double h[4];
     CK(c, cudaMemcpyAsync(h, c->out4, sizeof h, cudaMemcpyDeviceToHost, c->s_la));
     CK(c, cudaStreamSynchronize(c->s_la));
@@ -504,6 +624,45 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
 }
 
 int64_t hpl_launch_count(const hpl_ctx *c) { return c ? c->launches : 0; }
+
+hpl_status hpl_plan_iteration(int64_t N, int32_t NB, int32_t P, int32_t Q, int32_t myrow,
+                              int32_t mycol, int64_t j, int64_t *out8)
+{
+    if (!out8 || N < 1 || NB < 1 || P < 1 || Q < 1 || myrow < 0 || myrow >= P || mycol < 0 ||
+        mycol >= Q || j < 0 || j * NB >= N)
+        return HPL_ERR_ARG;
+    hpl_ctx t;
+    t.N = N; t.NB = NB; t.P = P; t.Q = Q; t.myrow = myrow; t.mycol = mycol;
+    t.mloc = numroc(N, NB, myrow, P);
+    t.nloc = numroc(N + 1, NB, mycol, Q);
+    const int64_t nblk = cdiv(N, NB);
+    const int64_t j0 = j * NB, jb = jb_of(&t, j);
+    const int64_t lct = lcols_before(&t, j0 + jb);
+    const bool has_next = j + 1 < nblk;
+    const int64_t jb1 = has_next ? jb_of(&t, j + 1) : 0;
+    const bool own_next = has_next && mycol == (int)((j + 1) % Q);
+    out8[0] = lrows_before(&t, j0);            // first active local row
+    out8[1] = lct;                             // first trailing local column
+    out8[2] = own_next ? lct : lct;            // look-ahead range begin
+    out8[3] = own_next ? lct + jb1 : lct;      // look-ahead range end
+    out8[4] = lct + (own_next ? jb1 : 0);      // rest range begin
+    out8[5] = t.nloc;                          // rest range end
+    out8[6] = (int)(j % Q) == mycol ? lcols_before(&t, j0) : -1;  // local panel column (owner)
+    out8[7] = jb;
+    return HPL_OK;
+}
+
+hpl_status hpl_pin_host(void *p, int64_t bytes, int32_t pin)
+{
+    if (!p || bytes <= 0) return HPL_ERR_ARG;
+    cudaError_t e = pin ? cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault)
+                        : cudaHostUnregister(p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return HPL_ERR_CUDA;
+    }
+    return HPL_OK;
+}
 
 hpl_status hpl_last_timing(const hpl_ctx *c, double *out6)
 {

@@ -92,11 +92,22 @@ cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src
                                  int64_t ldu);
 
 // ---------------------------------------------------------------- solve / residual
+// Single-matrix back solve (y = column N of U's rows): hplk_back_solve.
 cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,
                        const double *y, int64_t ystride, double *x, double *tbuf);
-// out4 (device, 4 doubles: rinf, anorm, xnorm, bnorm) for the seeded system.
-cudaError_t residual_seeded(cudaStream_t st, uint64_t seed, int64_t N, const double *x,
-                            double *out4);
+// partial[r] = sum_{lc_lo <= c < lc_hi} Urows[r][c] x[gcol(c)] - (lcy >= 0 ? Urows[r][lcy] : 0)
+cudaError_t bs_partial(cudaStream_t st, int nb, const double *Urows, int64_t ldu, int64_t lc_lo,
+                       int64_t lc_hi, int NB, int Q, int mycol, const double *x, int64_t lcy,
+                       double *partial);
+// xb = U_bb^{-1} (-partial)
+cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
+                    const double *partial, double *xb);
+// Residual of the seeded system: per-rank partial sums over local columns,
+// then (after the caller's all-reduce) the norms into out4 = {rinf, anorm, xnorm, bnorm}.
+cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int Q, int mycol,
+                             int64_t lcols, const double *x, double *r, double *a);
+cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, const double *r,
+                              const double *a, const double *x, double *out4);
 
 // FP64 tensor-pipe ceiling: register-resident DMMA chain on every SM.
 cudaError_t dmma_peak(int iters, int blocks_per_sm, int warps, double *ms, double *flop);

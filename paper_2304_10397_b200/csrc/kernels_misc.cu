@@ -212,17 +212,20 @@ cudaError_t trsm_cols(cudaStream_t st, int64_t k, int64_t ncols, const double *L
 }
 
 // ---------------------------------------------------------------- back solve
-// Blocked back substitution U x = y, bottom block first:
-//   t = y_b - U[b, right] x_right      (one CTA per row of the block)
-//   x_b = U_bb^{-1} t                  (one CTA; thread r owns row r)
-__global__ void bs_gemv_kernel(int64_t r0, int64_t r1, int64_t N, const double *__restrict__ U,
-                               int64_t ldu, const double *__restrict__ y, int64_t ystride,
-                               const double *__restrict__ x, double *t)
+// Blocked back substitution U x = y, bottom block first.
+// Columns of U may be distributed over Q process columns (block-cyclic); x is
+// replicated.  Per block b = rows [r0, r0+nb):
+//   partial[r] = sum_{local c : r1 <= gcol(c) < N} U[r][c] x[gcol(c)]  -  y[r] (y owner only)
+//   (summed over the process row), then x_b = U_bb^{-1} (-partial) on the
+//   owner of block column b.
+__global__ void bs_partial_kernel(const double *__restrict__ U, int64_t ldu, int64_t lc_lo,
+                                  int64_t lc_hi, int NB, int Q, int mycol,
+                                  const double *__restrict__ x, int64_t lcy, double *partial)
 {
-    const int64_t row = r0 + blockIdx.x;
-    const double *u = U + row * ldu;
+    const double *u = U + (int64_t)blockIdx.x * ldu;
     double s = 0.0;
-    for (int64_t c = r1 + threadIdx.x; c < N; c += blockDim.x) s += u[c] * x[c];
+    for (int64_t c = lc_lo + threadIdx.x; c < lc_hi; c += blockDim.x)
+        s += u[c] * x[l2g(c, NB, Q, mycol)];
     __shared__ double red[32];
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -230,38 +233,62 @@ __global__ void bs_gemv_kernel(int64_t r0, int64_t r1, int64_t N, const double *
     if (threadIdx.x < 32) {
         s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) t[blockIdx.x] = y[row * ystride] - s;
+        if (threadIdx.x == 0) partial[blockIdx.x] = s - (lcy >= 0 ? u[lcy] : 0.0);
     }
 }
 
 constexpr int BS_MAXB = 1024;
+// x[r0 + r] for r < nb from U_bb (rows of U starting at the block, columns
+// starting at the block's local column) and t = -partial.
 __global__ void __launch_bounds__(BS_MAXB)
-bs_diag_kernel(int64_t r0, int nb, const double *__restrict__ U, int64_t ldu,
-               const double *__restrict__ t, double *x)
+bs_diag_kernel(int nb, const double *__restrict__ Ubb, int64_t ldu,
+               const double *__restrict__ partial, double *xb)
 {
     __shared__ double xs[BS_MAXB];
     const int r = threadIdx.x;
-    double acc = r < nb ? t[r] : 0.0;
-    const double *urow = U + (r0 + r) * ldu + r0;
+    double acc = r < nb ? -partial[r] : 0.0;
+    const double *urow = Ubb + (int64_t)r * ldu;
     for (int i = nb - 1; i >= 0; --i) {
         if (r == i) xs[i] = acc / urow[i];
         __syncthreads();
         if (r < i) acc -= urow[i] * xs[i];
     }
-    if (r < nb) x[r0 + r] = xs[r];
+    if (r < nb) xb[r] = xs[r];
+}
+
+cudaError_t bs_partial(cudaStream_t st, int nb, const double *Urows, int64_t ldu, int64_t lc_lo,
+                       int64_t lc_hi, int NB, int Q, int mycol, const double *x, int64_t lcy,
+                       double *partial)
+{
+    if (nb <= 0) return cudaSuccess;
+    bs_partial_kernel<<<nb, 256, 0, st>>>(Urows, ldu, lc_lo, lc_hi, NB, Q, mycol, x, lcy, partial);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
+                    const double *partial, double *xb)
+{
+    if (nb <= 0) return cudaSuccess;
+    if (nb > BS_MAXB) return cudaErrorInvalidValue;
+    bs_diag_kernel<<<1, ((nb + 31) / 32) * 32, 0, st>>>(nb, Ubb, ldu, partial, xb);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,
                        const double *y, int64_t ystride, double *x, double *tbuf)
 {
+    // single-process form (U and y in one matrix, y = column N): used by hplk_back_solve
+    (void)ystride;
     if (NB > BS_MAXB) return cudaErrorInvalidValue;
     const int64_t nblk = cdiv(N, NB);
+    const int64_t lcy = y - U;  // y is column N of the same row-major matrix
     for (int64_t b = nblk - 1; b >= 0; --b) {
         const int64_t r0 = b * NB, r1 = std::min<int64_t>(N, r0 + NB);
         const int nb = (int)(r1 - r0);
-        bs_gemv_kernel<<<nb, 256, 0, st>>>(r0, r1, N, U, ldu, y, ystride, x, tbuf);
-        bs_diag_kernel<<<1, ((nb + 31) / 32) * 32, 0, st>>>(r0, nb, U, ldu, tbuf, x);
-        count_launch(2);
+        HPL_CUDA_TRY(bs_partial(st, nb, U + r0 * ldu, ldu, r1, N, NB, 1, 0, x, lcy, tbuf));
+        HPL_CUDA_TRY(bs_diag(st, nb, U + r0 * ldu + r0, ldu, tbuf, x + r0));
     }
     return cudaGetLastError();
 }
@@ -276,47 +303,82 @@ __device__ __forceinline__ void atomic_max_nonneg(double *addr, double v)
     atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
-__global__ void residual_kernel(uint64_t seed, int64_t N, const double *__restrict__ x,
-                                double *out4)
+// Per-rank part of r = A0 x - b0 over this rank's local columns (< N):
+// r[i] = sum_{local c} A0[i][gcol(c)] x[gcol(c)], a[i] = sum |A0[i][gcol(c)]|
+// (P = 1: all rows local).  Summed over the process row by the caller.
+__global__ void residual_partial_kernel(uint64_t seed, int64_t N, int NB, int Q, int mycol,
+                                        int64_t lcols, const double *__restrict__ x, double *r,
+                                        double *a)
 {
     const int64_t i = blockIdx.x;
-    double s = 0.0, a = 0.0;
-    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+    double s = 0.0, t = 0.0;
+    for (int64_t c = threadIdx.x; c < lcols; c += blockDim.x) {
+        const int64_t j = l2g(c, NB, Q, mycol);
         const double v = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)j);
         s = fma(v, x[j], s);
-        a += fabs(v);
+        t += fabs(v);
     }
     __shared__ double rs[32], ra[32];
     for (int o = 16; o; o >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
-        a += __shfl_xor_sync(0xffffffffu, a, o);
+        t += __shfl_xor_sync(0xffffffffu, t, o);
     }
-    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; ra[threadIdx.x >> 5] = a; }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; ra[threadIdx.x >> 5] = t; }
     __syncthreads();
     if (threadIdx.x < 32) {
         const bool ok = threadIdx.x < (blockDim.x >> 5);
         s = ok ? rs[threadIdx.x] : 0.0;
-        a = ok ? ra[threadIdx.x] : 0.0;
+        t = ok ? ra[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) {
             s += __shfl_xor_sync(0xffffffffu, s, o);
-            a += __shfl_xor_sync(0xffffffffu, a, o);
+            t += __shfl_xor_sync(0xffffffffu, t, o);
         }
-        if (threadIdx.x == 0) {
-            const double b = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)N);
-            atomic_max_nonneg(&out4[0], fabs(s - b));
-            atomic_max_nonneg(&out4[1], a);
-            atomic_max_nonneg(&out4[2], fabs(x[i]));
-            atomic_max_nonneg(&out4[3], fabs(b));
-        }
+        if (threadIdx.x == 0) { r[i] = s; a[i] = t; }
     }
 }
 
-cudaError_t residual_seeded(cudaStream_t st, uint64_t seed, int64_t N, const double *x,
-                            double *out4)
+// out4 = {max|r_i - b_i|, max a_i, max|x_i|, max|b_i|} (out4 zeroed by caller)
+__global__ void residual_finalize_kernel(uint64_t seed, int64_t N, const double *__restrict__ r,
+                                         const double *__restrict__ a,
+                                         const double *__restrict__ x, double *out4)
+{
+    double m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double b = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)N);
+        m0 = fmax(m0, fabs(r[i] - b));
+        m1 = fmax(m1, a[i]);
+        m2 = fmax(m2, fabs(x[i]));
+        m3 = fmax(m3, fabs(b));
+    }
+    for (int o = 16; o; o >>= 1) {
+        m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+        m3 = fmax(m3, __shfl_xor_sync(0xffffffffu, m3, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(&out4[0], m0);
+        atomic_max_nonneg(&out4[1], m1);
+        atomic_max_nonneg(&out4[2], m2);
+        atomic_max_nonneg(&out4[3], m3);
+    }
+}
+
+cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int Q, int mycol,
+                             int64_t lcols, const double *x, double *r, double *a)
+{
+    if (N > INT32_MAX) return cudaErrorInvalidValue;
+    residual_partial_kernel<<<(unsigned)N, 256, 0, st>>>(seed, N, NB, Q, mycol, lcols, x, r, a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, const double *r,
+                              const double *a, const double *x, double *out4)
 {
     HPL_CUDA_TRY(cudaMemsetAsync(out4, 0, 4 * sizeof(double), st));
-    if (N > INT32_MAX) return cudaErrorInvalidValue;
-    residual_kernel<<<(unsigned)N, 256, 0, st>>>(seed, N, x, out4);
+    residual_finalize_kernel<<<296, 256, 0, st>>>(seed, N, r, a, x, out4);
     count_launch();
     return cudaGetLastError();
 }

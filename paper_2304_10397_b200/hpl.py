@@ -166,6 +166,21 @@ def hpl_last_timing(ctx: Ctx) -> dict:
                 dgemm_flop=o[4], launches=int(o[5]))
 
 
+def hpl_plan_iteration(N: int, NB: int, P: int, Q: int, myrow: int, mycol: int, j: int) -> dict:
+    """Host-only bookkeeping of iteration j on process (myrow, mycol)."""
+    o = np.zeros(8, dtype=np.int64)
+    st = lib.hpl_plan_iteration(N, NB, P, Q, myrow, mycol, j, ptr(o))
+    if st != 0:
+        raise HplError(st, "hpl_plan_iteration: invalid arguments")
+    return dict(lr0=int(o[0]), lct=int(o[1]), la=(int(o[2]), int(o[3])), rest=(int(o[4]), int(o[5])),
+                lpanel=int(o[6]), jb=int(o[7]))
+
+
+def hpl_pin_host(arr: np.ndarray, pin: bool = True) -> bool:
+    """Page-lock a host array for DMA-speed copies; returns False if refused."""
+    return lib.hpl_pin_host(ptr(arr), arr.nbytes, 1 if pin else 0) == 0
+
+
 # ---------------------------------------------------------------- kernel-level
 def _k(st: int, what: str):
     if st != 0:

@@ -1,0 +1,80 @@
+"""Multi-rank HPL through the C ABI (one process per GPU).
+
+    torchrun --nproc-per-node Q --master-addr 127.0.0.1 --master-port PORT \\
+        tools/dist_hpl.py N NB P Q [seed] [--oracle] [--la 0|1]
+
+rank 0 creates the NCCL unique id (hpl_get_unique_id); it travels to the other
+ranks over a gloo process group; every rank then calls hpl_init_dist.  With
+--oracle, rank 0 compares the pivots and x with the CPU oracle.
+Prints one JSON line on rank 0; exit code 0 iff residual < 16 (and parity).
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    N, NB, P, Q = (int(v) for v in args[:4])
+    seed = int(args[4]) if len(args) > 4 else 42
+    la = 1
+    if "--la" in sys.argv:
+        la = int(sys.argv[sys.argv.index("--la") + 1])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    import paper_2304_10397_b200 as H
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        uid = torch.frombuffer(bytearray(H.hpl_get_unique_id()), dtype=torch.uint8)
+    dist.broadcast(uid, 0)
+    ctx = H.hpl_init_dist(N, NB, P, Q, seed, rank, world, bytes(uid.tolist()), local)
+    H.hpl_set_option(ctx, "lookahead", la)
+    dist.barrier()
+    t0 = time.perf_counter()
+    H.hpl_factor(ctx)
+    x = H.hpl_solve(ctx)
+    dist.barrier()
+    wall = time.perf_counter() - t0
+    tm = H.hpl_last_timing(ctx)
+    ipiv = H.hpl_get_ipiv(ctx)
+    r = H.hpl_residual(ctx)
+    H.hpl_free(ctx)
+    dev = torch.tensor([tm["factor_ms"] + tm["solve_ms"]], dtype=torch.float64)
+    dist.all_reduce(dev, op=dist.ReduceOp.MAX)
+    ok = r < 16.0
+    out = dict(N=N, NB=NB, P=P, Q=Q, resid=r, wall_s=wall, device_ms=float(dev.item()),
+               tflops=(2 / 3 * N ** 3 + 1.5 * N ** 2) / (float(dev.item()) * 1e-3) / 1e12)
+    if "--oracle" in sys.argv and rank == 0:
+        import oracle
+        o = oracle.run(N, seed)
+        out["ipiv_equal"] = bool(np.array_equal(ipiv, o["ipiv"]))
+        out["x_rel"] = float(np.max(np.abs(x - o["x"])) / np.max(np.abs(o["x"])))
+        out["oracle_resid"] = o["resid"]
+        ok = ok and out["ipiv_equal"] and out["x_rel"] <= 1e-9 and o["resid"] < 16.0
+    # every rank must hold the same x and pivots
+    xs = torch.from_numpy(x.copy())
+    x0 = xs.clone()
+    dist.broadcast(x0, 0)
+    out_same = bool(torch.equal(xs, x0))
+    flag = torch.tensor([1 if out_same else 0], dtype=torch.int64)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    out["x_replicated"] = bool(flag.item())
+    ok = ok and out["x_replicated"]
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
