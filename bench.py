@@ -119,6 +119,7 @@ def cpu_baseline(n: int, seed: int, reps: int = 1):
     """The oracle (plain GEPP + solves) on the host cores: factor+solve of the
     seeded N=n system; returns (TFLOP/s, seconds, threads, resid)."""
     import oracle
+    oracle.set_threads(len(os.sched_getaffinity(0)))   # torchrun exports OMP_NUM_THREADS=1
     best = None
     for _ in range(reps):
         A, b = oracle.generate(seed, n)

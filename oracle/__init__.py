@@ -77,6 +77,8 @@ def lib():
             L.oracle_maxloc.argtypes = [i64, dp, ip]
             L.oracle_residual_rows.restype = None
             L.oracle_residual_rows.argtypes = [i64, u64, dp, i64, ip, dp, dp]
+            L.oracle_set_threads.restype = None
+            L.oracle_set_threads.argtypes = [ctypes.c_int]
             L.oracle_num_threads.restype = ctypes.c_int
             L.oracle_num_threads.argtypes = []
             _lib = L
@@ -216,6 +218,10 @@ def maxloc(absval, rows):
     r = np.ascontiguousarray(rows, dtype=np.int64)
     k = int(lib().oracle_maxloc(len(a), _p(a), _p(r)))
     return float(a[k]), int(r[k])
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
 
 
 def num_threads() -> int:

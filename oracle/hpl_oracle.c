@@ -321,3 +321,13 @@ void oracle_residual_rows(int64_t N, uint64_t seed, const double *x, int64_t nro
         rsum[t] = a;
     }
 }
+
+/* Thread count for the row-parallel loops (results are thread-count invariant). */
+void oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
