@@ -38,6 +38,14 @@ struct hpl_ctx {
     int rank = 0, nranks = 1, myrow = 0, mycol = 0, device = 0;
     bool dist = false;
     ncclComm_t world = nullptr, row_comm = nullptr, col_comm = nullptr;
+    ncclComm_t col_comm_tr = nullptr;            // column comm used only by S_tr (RS of the rest)
+    // P > 1: replicated top block, RS buffers (one set per stream), pivot exchange
+    double *Tbuf = nullptr;
+    double *Ub[2] = {nullptr, nullptr}, *Wb[2] = {nullptr, nullptr};   // [0] = S_la, [1] = S_tr
+    void *xbuf = nullptr;
+    std::vector<void *> xpeer;
+    DistExchange xch{};
+    unsigned long long xseq = 0;
     double *rvec = nullptr, *avec = nullptr;   // residual partial sums (N each)
     // local storage
     int64_t mloc = 0, nloc = 0, lda = 0;
@@ -121,29 +129,57 @@ int64_t jb_of(const hpl_ctx *c, int64_t j) { return std::min<int64_t>(c->NB, c->
 // local rows (cols) of this process with global index < g
 int64_t lrows_before(const hpl_ctx *c, int64_t g) { return numroc(g, c->NB, c->myrow, c->P); }
 int64_t lcols_before(const hpl_ctx *c, int64_t g) { return numroc(g, c->NB, c->mycol, c->Q); }
-// leading dimension of the packed panel of iteration j (active local rows)
-int64_t panel_ld(const hpl_ctx *c, int64_t j)
+// Active local rows of iteration j: the block row j (owner process row only)
+// starts at local row lr0; the rows below it ("L rows") start at lrL0.
+int prow_of(const hpl_ctx *c, int64_t j) { return (int)(j % c->P); }
+int64_t lrL0_of(const hpl_ctx *c, int64_t j)
 {
-    return round_up(std::max<int64_t>(c->mloc - lrows_before(c, j * c->NB), 1), 16);
+    const int64_t lr0 = lrows_before(c, j * c->NB);
+    return lr0 + (c->myrow == prow_of(c, j) ? jb_of(c, j) : 0);
 }
+// The packed panel is [T; L]: T = the jb rows of block row j (replicated on
+// the whole process column when P > 1), then this process row's L rows.
+int64_t panel_rows(const hpl_ctx *c, int64_t j) { return jb_of(c, j) + (c->mloc - lrL0_of(c, j)); }
+int64_t panel_ld(const hpl_ctx *c, int64_t j) { return round_up(panel_rows(c, j), 16); }
 int64_t *panel_ipiv(hpl_ctx *c, int64_t j, int b)
 {
     // the panel buffer has one extra column; it carries the pivots through LBCAST
     return reinterpret_cast<int64_t *>(c->panel[b] + jb_of(c, j) * panel_ld(c, j));
 }
 
-// FACT(j) on the process column that owns panel j: pack the active local rows
-// of the panel columns (column-major), factor, write the factored panel back.
+// FACT(j) on the process column that owns panel j: pack [T; L] column-major,
+// factor, write the factored panel back to A.
 hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 {
-    const int64_t j0 = j * c->NB, jb = jb_of(c, j);
-    const int64_t lr0 = lrows_before(c, j0), mP = c->mloc - lr0, ldpj = panel_ld(c, j);
+    const int64_t j0 = j * c->NB, jb = jb_of(c, j), ldpj = panel_ld(c, j);
+    const int64_t lr0 = lrows_before(c, j0), lrL0 = lrL0_of(c, j), mL = c->mloc - lrL0;
     const int64_t lcp = lcols_before(c, j0);
-    double *Ablk = c->A + lr0 * c->lda + lcp;
-    CK(c, rm_to_cm(st, mP, jb, Ablk, c->lda, c->panel[b], ldpj));
-    CK(c, panel_fact(st, mP, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin, &c->fw,
-                     c->scratch, j0));
-    CK(c, cm_to_rm(st, mP, jb, c->panel[b], ldpj, Ablk, c->lda));
+    const bool is_prow = c->myrow == prow_of(c, j);
+    if (c->P == 1) {
+        // T and L are contiguous local rows [lr0, mloc)
+        double *Ablk = c->A + lr0 * c->lda + lcp;
+        CK(c, rm_to_cm(st, jb + mL, jb, Ablk, c->lda, c->panel[b], ldpj));
+        CK(c, panel_fact(st, jb + mL, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin,
+                         &c->fw, c->scratch, j0));
+        CK(c, cm_to_rm(st, jb + mL, jb, c->panel[b], ldpj, Ablk, c->lda));
+        return HPL_OK;
+    }
+    // T from the owner of block row j to the whole process column
+    if (is_prow) CK(c, rm_to_cm(st, jb, jb, c->A + lr0 * c->lda + lcp, c->lda, c->Tbuf, jb));
+    NK(c, ncclBroadcast(c->Tbuf, c->Tbuf, (size_t)(jb * jb), ncclDouble, prow_of(c, j),
+                        c->col_comm, st));
+    CK(c, cudaMemcpy2DAsync(c->panel[b], ldpj * 8, c->Tbuf, jb * 8, jb * 8, jb,
+                            cudaMemcpyDeviceToDevice, st));
+    CK(c, rm_to_cm(st, mL, jb, c->A + lrL0 * c->lda + lcp, c->lda, c->panel[b] + jb, ldpj));
+    DistFact df{};
+    df.dp.j0 = j0; df.dp.lrL0 = lrL0; df.dp.jbp = (int)jb; df.dp.is_prow = is_prow ? 1 : 0;
+    df.dp.NB = c->NB; df.dp.P = c->P; df.dp.myrow = c->myrow;
+    df.ex = c->xch;
+    df.seq = &c->xseq;
+    CK(c, panel_fact(st, jb + mL, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin, &c->fw,
+                     c->scratch, j0, &df));
+    CK(c, cm_to_rm(st, mL, jb, c->panel[b] + jb, ldpj, c->A + lrL0 * c->lda + lcp, c->lda));
+    if (is_prow) CK(c, cm_to_rm(st, jb, jb, c->panel[b], ldpj, c->A + lr0 * c->lda + lcp, c->lda));
     return HPL_OK;
 }
 
@@ -156,8 +192,8 @@ hpl_status lbcast_and_plan(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
     if (c->Q > 1)
         NK(c, ncclBroadcast(c->panel[b], c->panel[b], (size_t)((jb + 1) * ldpj), ncclDouble, pcol,
                             c->row_comm, st));
-    const int64_t lr0 = lrows_before(c, j0);
-    CK(c, pivot_plan(st, jb, lr0, panel_ipiv(c, j, b), j0, c->gpiv + j0, c->src[b], c->disp[b],
+    // the plan is in GLOBAL rows (P = 1: global == local)
+    CK(c, pivot_plan(st, jb, j0, panel_ipiv(c, j, b), j0, c->gpiv + j0, c->src[b], c->disp[b],
                      c->ndisp[b]));
     CK(c, trsm_cols(st, jb, jb, c->panel[b], ldpj, c->linv[b], c->ldlinv, true));
     return HPL_OK;
@@ -185,26 +221,55 @@ hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0
     if (ev) CK(c, cudaEventRecord(ev[0], st));
     const int slot = st == c->s_la ? SLOT_LOOKAHEAD : SLOT_TRAIL;
     const int64_t j0 = j * c->NB, jb = jb_of(c, j);
-    const int64_t lr0 = lrows_before(c, j0), ldpj = panel_ld(c, j);
+    const int64_t lr0 = lrows_before(c, j0), lrL0 = lrL0_of(c, j), ldpj = panel_ld(c, j);
+    const bool is_prow = c->myrow == prow_of(c, j);
+    const int64_t n = c1 - c0;
     double *u = c->U + ucol(c0), *u2 = c->U2 + ucol(c0);
-    double *top = c->A + lr0 * c->lda + c0;
-    if (c1 > c0)
+    int64_t ldub = c->ldu;
+    double *top = c->A + lr0 * c->lda + c0;   // block row j (owner process row only)
+    if (n > 0 && c->P == 1) {
         CK(c, laswp_gather_scatter(st, jb, c->src[b], c->disp[b], c->ndisp[b], jb, c->A, c->lda,
                                    c0, c1, u, c->ldu));
+    } else if (n > 0) {
+        // RS across the process column: U = the final block rows (each row from
+        // its owner, summed with zeros elsewhere), W = the original block row
+        // (from its owner) for the displaced rows.
+        const int sidx = st == c->s_la ? 0 : 1;
+        ncclComm_t comm = st == c->s_la ? c->col_comm : c->col_comm_tr;
+        ldub = round_up(n, 16);
+        u = c->Ub[sidx];
+        double *w = c->Wb[sidx];
+        CK(c, rs_pack(st, jb, c->src[b], c->A, c->lda, c0, c1, u, ldub, c->NB, c->P, c->myrow));
+        if (is_prow)
+            CK(c, cudaMemcpy2DAsync(w, ldub * 8, top, c->lda * 8, n * 8, jb,
+                                    cudaMemcpyDeviceToDevice, st));
+        NK(c, ncclGroupStart());
+        NK(c, ncclAllReduce(u, u, (size_t)(jb * ldub), ncclDouble, ncclSum, comm, st));
+        NK(c, ncclBroadcast(w, w, (size_t)(jb * ldub), ncclDouble, prow_of(c, j), comm, st));
+        NK(c, ncclGroupEnd());
+        CK(c, rs_scatter(st, c->disp[b], c->ndisp[b], w, ldub, j0, c->A, c->lda, c0, c1, c->NB,
+                         c->P, c->myrow));
+    }
     if (ev) CK(c, cudaEventRecord(ev[1], st));
-    // block row j <- L11^{-1} U  (written to A and to the aligned copy U2)
-    if (c1 > c0)
-        CK(c, dgemm(st, GEMM_ASSIGN, true, jb, c1 - c0, jb, c->linv[b], c->ldlinv, u, c->ldu,
-                    top, c->lda, -1, u2, c->ldu, slot));
+    // block row j <- L11^{-1} U: into U2 (the DGEMM operand) and, on the owner
+    // of block row j, into A as well
+    if (n > 0) {
+        if (is_prow)
+            CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, u, ldub, top,
+                        c->lda, -1, u2, c->ldu, slot));
+        else
+            CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, u, ldub, u2,
+                        c->ldu, -1, nullptr, 0, slot));
+    }
     if (ev) CK(c, cudaEventRecord(ev[2], st));
-    const int64_t mrest = c->mloc - lr0 - jb;
-    if (mrest > 0 && c1 > c0)
-        CK(c, dgemm(st, GEMM_UPDATE, false, mrest, c1 - c0, jb, c->panel[b] + jb, ldpj, u2,
-                    c->ldu, top + jb * c->lda, c->lda, -1, nullptr, 0, slot));
+    const int64_t mrest = c->mloc - lrL0;
+    if (mrest > 0 && n > 0)
+        CK(c, dgemm(st, GEMM_UPDATE, false, mrest, n, jb, c->panel[b] + jb, ldpj, u2, c->ldu,
+                    c->A + lrL0 * c->lda + c0, c->lda, -1, nullptr, 0, slot));
     if (ev) {
         CK(c, cudaEventRecord(ev[3], st));
-        if (mrest > 0 && c1 > c0) {
-            c->dgemm_flop += 2.0 * (double)mrest * (double)(c1 - c0) * (double)jb;
+        if (mrest > 0 && n > 0) {
+            c->dgemm_flop += 2.0 * (double)mrest * (double)n * (double)jb;
             c->dgemm_launches += 1;
         }
     }
@@ -236,7 +301,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     c->mloc = numroc(c->N, c->NB, c->myrow, c->P);
     c->nloc = numroc(c->N + 1, c->NB, c->mycol, c->Q);
     c->lda = round_up(std::max<int64_t>(c->nloc, 1), 16);
-    c->ldp = round_up(std::max<int64_t>(c->mloc, 1), 16);
+    c->ldp = round_up(std::max<int64_t>(c->mloc + (c->P > 1 ? c->NB : 0), 1), 16);
     c->ldlinv = round_up(c->NB, 16);
     c->ldu = round_up(c->nloc + 2, 16);
     auto M = [&](void **p, size_t bytes) -> bool {
@@ -264,8 +329,16 @@ hpl_status alloc_ctx(hpl_ctx *c)
     if (!M((void **)&c->x, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
     if (!M((void **)&c->tbuf, sizeof(double) * NBs)) return HPL_ERR_OOM;
     if (!M((void **)&c->out4, sizeof(double) * 4)) return HPL_ERR_OOM;
-    if (!M((void **)&c->rvec, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
-    if (!M((void **)&c->avec, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
+    if (!M((void **)&c->rvec, sizeof(double) * (size_t)std::max<int64_t>(c->mloc, 1))) return HPL_ERR_OOM;
+    if (!M((void **)&c->avec, sizeof(double) * (size_t)std::max<int64_t>(c->mloc, 1))) return HPL_ERR_OOM;
+    if (c->P > 1) {
+        const size_t rs = sizeof(double) * NBs * (size_t)round_up(c->nloc, 16);
+        if (!M((void **)&c->Tbuf, sizeof(double) * NBs * NBs)) return HPL_ERR_OOM;
+        for (int k = 0; k < 2; ++k) {
+            if (!M((void **)&c->Ub[k], rs)) return HPL_ERR_OOM;
+            if (!M((void **)&c->Wb[k], rs)) return HPL_ERR_OOM;
+        }
+    }
     CK(c, fact_work_alloc(&c->fw));
     int lo, hi;
     CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -297,6 +370,11 @@ void release(hpl_ctx *c)
     }
     cudaFree(c->gpiv); cudaFree(c->U); cudaFree(c->U2); cudaFree(c->scratch);
     cudaFree(c->x); cudaFree(c->tbuf); cudaFree(c->out4); cudaFree(c->rvec); cudaFree(c->avec);
+    cudaFree(c->Tbuf);
+    for (int k = 0; k < 2; ++k) { cudaFree(c->Ub[k]); cudaFree(c->Wb[k]); }
+    for (void *pp : c->xpeer) if (pp) cudaIpcCloseMemHandle(pp);
+    cudaFree(c->xbuf);
+    if (c->col_comm_tr) ncclCommDestroy(c->col_comm_tr);
     if (c->row_comm) ncclCommDestroy(c->row_comm);
     if (c->col_comm) ncclCommDestroy(c->col_comm);
     if (c->world) ncclCommDestroy(c->world);
@@ -307,6 +385,44 @@ void release(hpl_ctx *c)
         if (c->ev_t[k]) cudaEventDestroy(c->ev_t[k]);
     if (c->s_la) cudaStreamDestroy(c->s_la);
     if (c->s_tr) cudaStreamDestroy(c->s_tr);
+}
+
+// P > 1: pivot-exchange areas shared inside each process column through CUDA
+// IPC (peer memory over NVLink); handles travel over the column communicator.
+hpl_status setup_exchange(hpl_ctx *c)
+{
+    const int P = c->P;
+    const int recd = 2 + c->NB;
+    const size_t rec_bytes = sizeof(double) * 2 * (size_t)P * recd;
+    const size_t bytes = rec_bytes + sizeof(unsigned long long) * 2 * P;
+    CK(c, cudaMalloc(&c->xbuf, bytes));
+    CK(c, cudaMemset(c->xbuf, 0, bytes));
+    cudaIpcMemHandle_t h;
+    CK(c, cudaIpcGetMemHandle(&h, c->xbuf));
+    char *dh = nullptr;
+    CK(c, cudaMalloc(&dh, sizeof(h) * P));
+    CK(c, cudaMemcpy(dh + sizeof(h) * c->myrow, &h, sizeof(h), cudaMemcpyHostToDevice));
+    NK(c, ncclAllGather(dh + sizeof(h) * c->myrow, dh, sizeof(h), ncclChar, c->col_comm, c->s_la));
+    CK(c, cudaStreamSynchronize(c->s_la));
+    std::vector<cudaIpcMemHandle_t> hs(P);
+    CK(c, cudaMemcpy(hs.data(), dh, sizeof(h) * P, cudaMemcpyDeviceToHost));
+    cudaFree(dh);
+    c->xpeer.assign(P, nullptr);
+    c->xch.P = P;
+    c->xch.myrow = c->myrow;
+    c->xch.recd = recd;
+    for (int p = 0; p < P; ++p) {
+        void *base = c->xbuf;
+        if (p != c->myrow) {
+            CK(c, cudaIpcOpenMemHandle(&c->xpeer[p], hs[p], cudaIpcMemLazyEnablePeerAccess));
+            base = c->xpeer[p];
+        }
+        c->xch.rec[p] = static_cast<double *>(base);
+        c->xch.flag[p] = reinterpret_cast<unsigned long long *>(static_cast<char *>(base) + rec_bytes);
+    }
+    c->xch.my_rec = c->xch.rec[c->myrow];
+    c->xch.my_flag = c->xch.flag[c->myrow];
+    return HPL_OK;
 }
 
 hpl_status check_args(int64_t N, int32_t NB, int32_t P, int32_t Q)
@@ -344,7 +460,7 @@ hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t s
     *out = nullptr;
     if (check_args(N, NB, P, Q) != HPL_OK || P * Q != nranks || rank < 0 || rank >= nranks)
         return HPL_ERR_ARG;
-    if (P != 1) return HPL_ERR_ARG;  // P > 1 (pivot exchange / RS) not built yet: DESIGN.md §6
+    if (P > MAX_P) return HPL_ERR_ARG;
     hpl_ctx *c = new hpl_ctx();
     *out = c;
     c->N = N; c->NB = NB; c->P = P; c->Q = Q; c->seed = seed;
@@ -357,7 +473,9 @@ hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t s
     NK(c, ncclCommInitRank(&c->world, nranks, id, rank));
     NK(c, ncclCommSplit(c->world, c->myrow, c->mycol, &c->row_comm, nullptr));
     NK(c, ncclCommSplit(c->world, c->mycol, c->myrow, &c->col_comm, nullptr));
+    NK(c, ncclCommSplit(c->world, c->mycol, c->myrow, &c->col_comm_tr, nullptr));
     hpl_status s = alloc_ctx(c);
+    if (s == HPL_OK && P > 1) s = setup_exchange(c);
     if (s == HPL_OK) s = generate(c);
     return s;
 }
@@ -482,7 +600,11 @@ hpl_status hpl_solve(hpl_ctx *c, double *x_host)
     const int64_t l0 = g_launches.load();
     CK(c, cudaEventRecord(c->ev_t[1], c->s_la));
     {
-        // distributed block back substitution over the process row (P = 1)
+        // Distributed block back substitution.  Block row bb lives on process
+        // row rb = bb mod P: its Q processes form the partial sums over their
+        // local columns (all-reduce on the row comm), the owner of the
+        // diagonal block (rb, bb mod Q) solves it, and x_b is broadcast to
+        // every rank (world comm) so x stays replicated.
         const int64_t N = c->N, nblk = cdiv(N, c->NB);
         const int ycol = (int)((N / c->NB) % c->Q);            // owner of global column N
         const int64_t lcy = c->mycol == ycol ? lcols_before(c, N) : -1;
@@ -490,19 +612,21 @@ hpl_status hpl_solve(hpl_ctx *c, double *x_host)
         for (int64_t bb = nblk - 1; bb >= 0; --bb) {
             const int64_t r0 = bb * c->NB, r1 = std::min<int64_t>(N, r0 + c->NB);
             const int nb = (int)(r1 - r0);
-            const int64_t lr0 = lrows_before(c, r0);
-            CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda, lcols_before(c, r1), lcN,
-                             c->NB, c->Q, c->mycol, c->x, lcy, c->tbuf));
-            if (c->Q > 1)
-                NK(c, ncclAllReduce(c->tbuf, c->tbuf, nb, ncclDouble, ncclSum, c->row_comm,
-                                    c->s_la));
-            const int owner = (int)(bb % c->Q);
-            if (c->mycol == owner)
-                CK(c, bs_diag(c->s_la, nb, c->A + lr0 * c->lda + lcols_before(c, r0), c->lda,
-                              c->tbuf, c->x + r0));
-            if (c->Q > 1)
-                NK(c, ncclBroadcast(c->x + r0, c->x + r0, nb, ncclDouble, owner, c->row_comm,
-                                    c->s_la));
+            const int rb = (int)(bb % c->P), qb = (int)(bb % c->Q);
+            if (c->myrow == rb) {
+                const int64_t lr0 = lrows_before(c, r0);
+                CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda, lcols_before(c, r1),
+                                 lcN, c->NB, c->Q, c->mycol, c->x, lcy, c->tbuf));
+                if (c->Q > 1)
+                    NK(c, ncclAllReduce(c->tbuf, c->tbuf, nb, ncclDouble, ncclSum, c->row_comm,
+                                        c->s_la));
+                if (c->mycol == qb)
+                    CK(c, bs_diag(c->s_la, nb, c->A + lr0 * c->lda + lcols_before(c, r0), c->lda,
+                                  c->tbuf, c->x + r0));
+            }
+            if (c->dist)
+                NK(c, ncclBroadcast(c->x + r0, c->x + r0, nb, ncclDouble, rb + qb * c->P,
+                                    c->world, c->s_la));
         }
     }
     if (x_host)
@@ -523,13 +647,18 @@ hpl_status hpl_residual(hpl_ctx *c, double *resid)
         set_err(c, "hpl_residual: call hpl_solve first");
         return HPL_ERR_STATE;
     }
-    CK(c, residual_partial(c->s_la, c->seed, c->N, c->NB, c->Q, c->mycol, lcols_before(c, c->N),
-                           c->x, c->rvec, c->avec));
+    // r and the row sums of |A0| for this process row's rows, summed over the
+    // process row; the norms are then maxed over the process column.
+    CK(c, residual_partial(c->s_la, c->seed, c->N, c->NB, c->P, c->myrow, c->mloc, c->Q,
+                           c->mycol, lcols_before(c, c->N), c->x, c->rvec, c->avec));
     if (c->Q > 1) {
-        NK(c, ncclAllReduce(c->rvec, c->rvec, c->N, ncclDouble, ncclSum, c->row_comm, c->s_la));
-        NK(c, ncclAllReduce(c->avec, c->avec, c->N, ncclDouble, ncclSum, c->row_comm, c->s_la));
+        NK(c, ncclAllReduce(c->rvec, c->rvec, c->mloc, ncclDouble, ncclSum, c->row_comm, c->s_la));
+        NK(c, ncclAllReduce(c->avec, c->avec, c->mloc, ncclDouble, ncclSum, c->row_comm, c->s_la));
     }
-    CK(c, residual_finalize(c->s_la, c->seed, c->N, c->rvec, c->avec, c->x, c->out4));
+    CK(c, residual_finalize(c->s_la, c->seed, c->N, c->NB, c->P, c->myrow, c->mloc, c->rvec,
+                            c->avec, c->x, c->out4));
+    if (c->dist)
+        NK(c, ncclAllReduce(c->out4, c->out4, 4, ncclDouble, ncclMax, c->world, c->s_la));
     double h[4];
     CK(c, cudaMemcpyAsync(h, c->out4, sizeof h, cudaMemcpyDeviceToHost, c->s_la));
     CK(c, cudaStreamSynchronize(c->s_la));

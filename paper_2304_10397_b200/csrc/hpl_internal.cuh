@@ -62,7 +62,33 @@ struct FactWork {
     double *cand;        // candidate records (2 parity buffers)
     unsigned *bar;       // grid barrier words (count, generation)
     int64_t *info;       // first singular global column; all-ones (== -1) if none
+    double *win;         // P > 1: winning pivot record (global row + full panel row)
+    double *tsnap;       // P > 1: snapshot of the replicated top row kc
     int max_ctas;
+};
+
+// P > 1 panel FACT: the P processes of the panel's process column exchange
+// pivot candidates (value, global row, full panel row) through peer memory
+// (CUDA IPC over NVLink) inside the leaf kernel.
+constexpr int MAX_P = 8;
+struct DistExchange {
+    double *rec[MAX_P];                 // record area on each peer (index = process row)
+    unsigned long long *flag[MAX_P];    // flag area on each peer
+    double *my_rec;                     // = rec[myrow]
+    unsigned long long *my_flag;        // = flag[myrow]
+    int P, myrow, recd;                 // recd = doubles per record (2 + NB)
+};
+// Panel rows [0, jbp) are the replicated top block T (global rows j0..j0+jbp);
+// rows jbp.. are this process row's other active rows, the first being local
+// row lrL0 (global row via the block-cyclic map with NB, P, myrow).
+struct DistPanel {
+    long long j0, lrL0;
+    int jbp, is_prow, NB, P, myrow;
+};
+struct DistFact {
+    DistPanel dp;
+    DistExchange ex;
+    unsigned long long *seq;            // host counter, advanced once per panel column
 };
 cudaError_t fact_work_alloc(FactWork *w);
 // Pivot winner among n candidates (max |v|, ties -> smallest row), as the FACT reduces.
@@ -74,7 +100,8 @@ void fact_work_free(FactWork *w);
 // transposed U block of the recursion GEMMs (>= nb*nb doubles).  A zero pivot
 // at panel column k records min(goff + k) in w->info.
 cudaError_t panel_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp,
-                       int64_t *ipiv_dev, int nbmin, FactWork *w, double *scratch, int64_t goff);
+                       int64_t *ipiv_dev, int nbmin, FactWork *w, double *scratch, int64_t goff,
+                       DistFact *dist = nullptr);
 
 // ---------------------------------------------------------------- LASWP
 // From panel-relative pivots (jb entries; positions r0+k <-> r0+ipiv_rel[k])
@@ -91,6 +118,16 @@ cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src
                                  double *A, int64_t lda, int64_t c0, int64_t c1, double *U,
                                  int64_t ldu);
 
+// P > 1 row swaps (RS): pack the rows of U this process row owns (zeros
+// elsewhere; summed over the process column by the caller), and scatter the
+// displaced rows from W = the original block row (broadcast from its owner).
+// src / disp hold GLOBAL rows; NB, P, myrow give the global->local row map.
+cudaError_t rs_pack(cudaStream_t st, int64_t jb, const int64_t *src, const double *A, int64_t lda,
+                    int64_t c0, int64_t c1, double *U, int64_t ldu, int NB, int P, int myrow);
+cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, const double *W,
+                       int64_t ldw, int64_t j0, double *A, int64_t lda, int64_t c0, int64_t c1,
+                       int NB, int P, int myrow);
+
 // ---------------------------------------------------------------- solve / residual
 // Single-matrix back solve (y = column N of U's rows): hplk_back_solve.
 cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,
@@ -102,12 +139,15 @@ cudaError_t bs_partial(cudaStream_t st, int nb, const double *Urows, int64_t ldu
 // xb = U_bb^{-1} (-partial)
 cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
                     const double *partial, double *xb);
-// Residual of the seeded system: per-rank partial sums over local columns,
-// then (after the caller's all-reduce) the norms into out4 = {rinf, anorm, xnorm, bnorm}.
-cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int Q, int mycol,
-                             int64_t lcols, const double *x, double *r, double *a);
-cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, const double *r,
-                              const double *a, const double *x, double *out4);
+// Residual of the seeded system: per-rank partial sums (local rows x local
+// columns), then (after the caller's all-reduce over the process row) the
+// norms into out4 = {rinf, anorm, xnorm, bnorm} (max over local rows).
+cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
+                             int64_t mloc, int Q, int mycol, int64_t lcols, const double *x,
+                             double *r, double *a);
+cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
+                              int64_t mloc, const double *r, const double *a, const double *x,
+                              double *out4);
 
 // FP64 tensor-pipe ceiling: register-resident DMMA chain on every SM.
 cudaError_t dmma_peak(int iters, int blocks_per_sm, int warps, double *ms, double *flop);

@@ -200,6 +200,177 @@ __global__ void panel_laswp_kernel(int nb, int64_t ldp, double *P, int k0, int w
     }
 }
 
+// ---------------------------------------------------------------- P > 1 leaf
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Leaf of the distributed panel: as leaf_fact_kernel, but the candidate search
+// spans the process column.  Per column: local candidates -> grid barrier ->
+// CTA 0 publishes (|v|, global row, the full panel row) into every peer's
+// record slot and raises its flag, waits for all P flags, picks the winner
+// (max |v|, smallest global row) and snapshots the replicated top row kc ->
+// grid barrier -> full-width swap on the owners -> rank-1 update of the leaf
+// columns.  The top block T is replicated on all P processes and updated
+// identically by each, so only the winner's payload crosses NVLink.
+__global__ void __launch_bounds__(FACT_THREADS)
+leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ipiv, double *cand,
+                      double *win, double *tsnap, unsigned *bar, unsigned long long *info,
+                      DistPanel dp, DistExchange ex, unsigned long long seq0)
+{
+    const unsigned G = gridDim.x;
+    const int chunk = (m + (int)G - 1) / (int)G;
+    const int rbeg = (int)blockIdx.x * chunk;
+    const int rend = min(m, rbeg + chunk);
+    const int jbp = dp.jbp;
+    __shared__ double s_v[FACT_THREADS / 32];
+    __shared__ long long s_g[FACT_THREADS / 32];
+    __shared__ int s_r[FACT_THREADS / 32];
+    __shared__ double s_pay[1024], s_ts[1024];
+    __shared__ long long s_win;
+    auto grow = [&](int r) -> long long {
+        if (r < jbp) return dp.j0 + r;
+        const long long l = dp.lrL0 + (r - jbp);
+        return ((l / dp.NB) * dp.P + dp.myrow) * dp.NB + l % dp.NB;
+    };
+    for (int kk = 0; kk < w; ++kk) {
+        const int kc = k0 + kk;
+        const unsigned long long seq = seq0 + kk + 1;
+        const int par = (int)(seq & 1);
+        double *rec = cand + (size_t)(kk & 1) * (MAX_CTAS + 1) * REC;
+        // ---- 1. local candidates (T rows count on the owner of block row j only)
+        double bv = -1.0;
+        long long bg = LLONG_MAX;
+        int br = -1;
+        const double *colk = Pn + (int64_t)kc * ldp;
+        for (int r = max(rbeg, kc) + threadIdx.x; r < rend; r += FACT_THREADS) {
+            if (r < jbp && !dp.is_prow) continue;
+            const double v = fabs(colk[r]);
+            const long long g = grow(r);
+            if (better(v, g, bv, bg)) { bv = v; bg = g; br = r; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const long long og = __shfl_xor_sync(0xffffffffu, bg, o);
+            const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+            if (better(ov, og, bv, bg)) { bv = ov; bg = og; br = orr; }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_v[threadIdx.x >> 5] = bv; s_g[threadIdx.x >> 5] = bg; s_r[threadIdx.x >> 5] = br;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 1; q < FACT_THREADS / 32; ++q)
+                if (better(s_v[q], s_g[q], bv, bg)) { bv = s_v[q]; bg = s_g[q]; br = s_r[q]; }
+            double *myrec = rec + (size_t)blockIdx.x * REC;
+            myrec[0] = bv;
+            myrec[1] = __longlong_as_double(bg);
+            myrec[2] = __longlong_as_double((long long)br);
+        }
+        __threadfence();
+        grid_barrier(bar, G);
+
+        // ---- 3. CTA 0: process-column exchange
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) {
+                bv = -1.0; bg = LLONG_MAX; br = -1;
+                for (unsigned c = 0; c < G; ++c) {
+                    const double v = __ldcg(rec + (size_t)c * REC);
+                    const long long g = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
+                    if (g != LLONG_MAX && better(v, g, bv, bg)) {
+                        bv = v; bg = g;
+                        br = (int)__double_as_longlong(__ldcg(rec + (size_t)c * REC + 2));
+                    }
+                }
+                s_v[0] = bv; s_g[0] = bg; s_r[0] = br;
+            }
+            __syncthreads();
+            bv = s_v[0]; bg = s_g[0]; br = s_r[0];
+            const size_t slot = ((size_t)par * ex.P + ex.myrow) * ex.recd;
+            for (int p = 0; p < ex.P; ++p) {
+                double *dst = ex.rec[p] + slot;
+                for (int c = threadIdx.x; c < jbp; c += FACT_THREADS)
+                    dst[2 + c] = br >= 0 ? __ldcg(Pn + (int64_t)c * ldp + br) : 0.0;
+                if (threadIdx.x == 0) {
+                    dst[0] = bv;
+                    dst[1] = __longlong_as_double(bg);
+                }
+            }
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS)
+                tsnap[c] = __ldcg(Pn + (int64_t)c * ldp + kc);
+            __threadfence_system();
+            __syncthreads();
+            if (threadIdx.x < ex.P) st_release_sys(ex.flag[threadIdx.x] + (size_t)par * ex.P + ex.myrow, seq);
+            if (threadIdx.x < ex.P)
+                while (ld_acquire_sys(ex.my_flag + (size_t)par * ex.P + threadIdx.x) != seq) {
+                }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int wslot = -1;
+                bv = -1.0; bg = LLONG_MAX;
+                for (int p = 0; p < ex.P; ++p) {
+                    const double *r = ex.my_rec + ((size_t)par * ex.P + p) * ex.recd;
+                    const double v = __ldcv(r);
+                    const long long g = __double_as_longlong(__ldcv(r + 1));
+                    if (g != LLONG_MAX && better(v, g, bv, bg)) { bv = v; bg = g; wslot = p; }
+                }
+                s_r[0] = wslot;
+                win[0] = __longlong_as_double(bg);
+            }
+            __syncthreads();
+            const double *wr = ex.my_rec + ((size_t)par * ex.P + s_r[0]) * ex.recd;
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) win[2 + c] = __ldcv(wr + 2 + c);
+            __threadfence();
+        }
+        grid_barrier(bar, G);
+
+        // ---- 5. full-width swap on the owners of the two rows
+        if (threadIdx.x == 0) s_win = __double_as_longlong(__ldcg(win));
+        for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+            s_pay[c] = __ldcg(win + 2 + c);
+            s_ts[c] = __ldcg(tsnap + c);
+        }
+        __syncthreads();
+        const long long gw = s_win;
+        const long long t = gw - dp.j0;
+        if (kc >= rbeg && kc < rend)
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) Pn[(int64_t)c * ldp + kc] = s_pay[c];
+        long long rswap = -1;
+        if (t >= 0 && t < jbp) {
+            if (t != kc) rswap = t;
+        } else if ((int)((gw / dp.NB) % dp.P) == dp.myrow) {
+            const long long l = (gw / ((long long)dp.NB * dp.P)) * dp.NB + gw % dp.NB;
+            rswap = jbp + (l - dp.lrL0);
+        }
+        if (rswap >= rbeg && rswap < rend)
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) Pn[(int64_t)c * ldp + rswap] = s_ts[c];
+        const double piv = s_pay[kc];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ipiv[kc] = t;
+            if (piv == 0.0) atomicMin(info, (unsigned long long)(dp.j0 + kc));
+        }
+        __syncthreads();
+        // ---- 6. scale column kc and rank-1 update of the leaf columns (own rows > kc)
+        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += FACT_THREADS) {
+            const double l = Pn[(int64_t)kc * ldp + r] / piv;
+            Pn[(int64_t)kc * ldp + r] = l;
+            for (int c = kk + 1; c < w; ++c) {
+                double *q = Pn + (int64_t)(k0 + c) * ldp + r;
+                *q = fma(-l, s_pay[k0 + c], *q);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 int g_num_sms = 0;
 
 cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
@@ -225,11 +396,37 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int 
     return cudaSuccess;
 }
 
+cudaError_t launch_leaf_dist(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
+                             int64_t *ipiv, FactWork *wk, DistFact *df)
+{
+    if (!g_num_sms) {
+        int dev;
+        HPL_CUDA_TRY(cudaGetDevice(&dev));
+        HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (df->dp.jbp > 1024) return cudaErrorInvalidValue;
+    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(m, 512)), g_num_sms);
+    G = std::min(G, wk->max_ctas);
+    int m_i = (int)m;
+    int64_t ldp_ = ldp;
+    int k0_ = k0, w_ = w;
+    unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
+    unsigned long long seq0 = *df->seq;
+    void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->win, &wk->tsnap,
+                    &wk->bar, &info, &df->dp, &df->ex, &seq0};
+    HPL_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)leaf_fact_dist_kernel, dim3(G),
+                                             dim3(FACT_THREADS), args, 0, st));
+    *df->seq += (unsigned long long)w;
+    count_launch();
+    return cudaSuccess;
+}
+
 cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp, int c0,
                      int w, int64_t *ipiv, int nbmin, FactWork *wk, double *scratch,
-                     long long goff)
+                     long long goff, DistFact *df)
 {
     if (w <= nbmin || w <= 2) {
+        if (df) return launch_leaf_dist(st, m, P, ldp, c0, w, ipiv, wk, df);  // full-width swaps
         HPL_CUDA_TRY(launch_leaf(st, m, P, ldp, c0, w, ipiv, wk, goff));
         if (nb > w) {
             panel_laswp_kernel<<<(unsigned)cdiv(nb, 128), 128, 0, st>>>((int)nb, ldp, P, c0, w,
@@ -242,7 +439,7 @@ cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t 
     // NDIV = 2; the split is rounded down to an even width so
     // every recursion offset stays 16-byte aligned for the TMA operands.
     const int w1 = std::max(2, (w / 2) & ~1), w2 = w - w1;
-    HPL_CUDA_TRY(rec_fact(st, m, nb, P, ldp, c0, w1, ipiv, nbmin, wk, scratch, goff));
+    HPL_CUDA_TRY(rec_fact(st, m, nb, P, ldp, c0, w1, ipiv, nbmin, wk, scratch, goff, df));
     // U12 <- L11^{-1} U12 (rows c0..c0+w1, cols c0+w1..c0+w)
     HPL_CUDA_TRY(trsm_cols(st, w1, w2, P + (int64_t)c0 * ldp + c0, ldp,
                            P + (int64_t)(c0 + w1) * ldp + c0, ldp, false));
@@ -257,7 +454,7 @@ cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t 
                            P + (int64_t)(c0 + w1) * ldp + c0 + w1, ldp, -1, nullptr, 0,
                            SLOT_FACT));
     }
-    return rec_fact(st, m, nb, P, ldp, c0 + w1, w2, ipiv, nbmin, wk, scratch, goff);
+    return rec_fact(st, m, nb, P, ldp, c0 + w1, w2, ipiv, nbmin, wk, scratch, goff, df);
 }
 
 // a8 as a standalone kernel (tests): the FACT's candidate reduction rule.
@@ -296,6 +493,8 @@ cudaError_t fact_work_alloc(FactWork *w)
     HPL_CUDA_TRY(cudaMemset(w->bar, 0, 64));
     HPL_CUDA_TRY(cudaMalloc(&w->info, sizeof(int64_t)));
     HPL_CUDA_TRY(cudaMemset(w->info, 0xff, sizeof(int64_t)));
+    HPL_CUDA_TRY(cudaMalloc(&w->win, sizeof(double) * (1024 + 2)));
+    HPL_CUDA_TRY(cudaMalloc(&w->tsnap, sizeof(double) * 1024));
     return cudaSuccess;
 }
 
@@ -304,18 +503,23 @@ void fact_work_free(FactWork *w)
     cudaFree(w->cand);
     cudaFree(w->bar);
     cudaFree(w->info);
+    cudaFree(w->win);
+    cudaFree(w->tsnap);
+    w->win = nullptr;
+    w->tsnap = nullptr;
     w->cand = nullptr;
     w->bar = nullptr;
     w->info = nullptr;
 }
 
 cudaError_t panel_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp,
-                       int64_t *ipiv_dev, int nbmin, FactWork *w, double *scratch, int64_t goff)
+                       int64_t *ipiv_dev, int nbmin, FactWork *w, double *scratch, int64_t goff,
+                       DistFact *dist)
 {
     if (nbmin < 1 || nbmin > LEAF_MAX) return cudaErrorInvalidValue;
-    if (m < nb || nb <= 0) return cudaErrorInvalidValue;
+    if (nb <= 0 || (!dist && m < nb)) return cudaErrorInvalidValue;
     if (m > INT32_MAX) return cudaErrorInvalidValue;
-    return rec_fact(st, m, nb, P, ldp, 0, (int)nb, ipiv_dev, nbmin, w, scratch, goff);
+    return rec_fact(st, m, nb, P, ldp, 0, (int)nb, ipiv_dev, nbmin, w, scratch, goff, dist);
 }
 
 }  // namespace hpl

@@ -303,14 +303,15 @@ __device__ __forceinline__ void atomic_max_nonneg(double *addr, double v)
     atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
-// Per-rank part of r = A0 x - b0 over this rank's local columns (< N):
-// r[i] = sum_{local c} A0[i][gcol(c)] x[gcol(c)], a[i] = sum |A0[i][gcol(c)]|
-// (P = 1: all rows local).  Summed over the process row by the caller.
-__global__ void residual_partial_kernel(uint64_t seed, int64_t N, int NB, int Q, int mycol,
-                                        int64_t lcols, const double *__restrict__ x, double *r,
-                                        double *a)
+// Per-rank part of r = A0 x - b0: for each LOCAL row (global row via the
+// block-cyclic map), r[l] = sum_{local c < N} A0[gi][gcol(c)] x[gcol(c)] and
+// a[l] = sum |A0[gi][gcol(c)]|; summed over the process row by the caller.
+__global__ void residual_partial_kernel(uint64_t seed, int64_t N, int NB, int P, int myrow, int Q,
+                                        int mycol, int64_t lcols, const double *__restrict__ x,
+                                        double *r, double *a)
 {
-    const int64_t i = blockIdx.x;
+    const int64_t l = blockIdx.x;
+    const int64_t i = l2g(l, NB, P, myrow);
     double s = 0.0, t = 0.0;
     for (int64_t c = threadIdx.x; c < lcols; c += blockDim.x) {
         const int64_t j = l2g(c, NB, Q, mycol);
@@ -333,24 +334,28 @@ __global__ void residual_partial_kernel(uint64_t seed, int64_t N, int NB, int Q,
             s += __shfl_xor_sync(0xffffffffu, s, o);
             t += __shfl_xor_sync(0xffffffffu, t, o);
         }
-        if (threadIdx.x == 0) { r[i] = s; a[i] = t; }
+        if (threadIdx.x == 0) { r[l] = s; a[l] = t; }
     }
 }
 
-// out4 = {max|r_i - b_i|, max a_i, max|x_i|, max|b_i|} (out4 zeroed by caller)
-__global__ void residual_finalize_kernel(uint64_t seed, int64_t N, const double *__restrict__ r,
+// out4 = {max|r_l - b_gi|, max a_l, max|x_i|, max|b_i|} over local rows
+// (x over all N: it is replicated).  out4 zeroed here.
+__global__ void residual_finalize_kernel(uint64_t seed, int64_t N, int NB, int P, int myrow,
+                                         int64_t mloc, const double *__restrict__ r,
                                          const double *__restrict__ a,
                                          const double *__restrict__ x, double *out4)
 {
     double m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < mloc; l += stride) {
+        const int64_t i = l2g(l, NB, P, myrow);
         const double b = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)N);
-        m0 = fmax(m0, fabs(r[i] - b));
-        m1 = fmax(m1, a[i]);
-        m2 = fmax(m2, fabs(x[i]));
+        m0 = fmax(m0, fabs(r[l] - b));
+        m1 = fmax(m1, a[l]);
         m3 = fmax(m3, fabs(b));
     }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += stride)
+        m2 = fmax(m2, fabs(x[i]));
     for (int o = 16; o; o >>= 1) {
         m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
         m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
@@ -365,20 +370,24 @@ __global__ void residual_finalize_kernel(uint64_t seed, int64_t N, const double 
     }
 }
 
-cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int Q, int mycol,
-                             int64_t lcols, const double *x, double *r, double *a)
+cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
+                             int64_t mloc, int Q, int mycol, int64_t lcols, const double *x,
+                             double *r, double *a)
 {
-    if (N > INT32_MAX) return cudaErrorInvalidValue;
-    residual_partial_kernel<<<(unsigned)N, 256, 0, st>>>(seed, N, NB, Q, mycol, lcols, x, r, a);
+    if (mloc <= 0) return cudaSuccess;
+    if (mloc > INT32_MAX) return cudaErrorInvalidValue;
+    residual_partial_kernel<<<(unsigned)mloc, 256, 0, st>>>(seed, N, NB, P, myrow, Q, mycol, lcols,
+                                                            x, r, a);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, const double *r,
-                              const double *a, const double *x, double *out4)
+cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
+                              int64_t mloc, const double *r, const double *a, const double *x,
+                              double *out4)
 {
     HPL_CUDA_TRY(cudaMemsetAsync(out4, 0, 4 * sizeof(double), st));
-    residual_finalize_kernel<<<296, 256, 0, st>>>(seed, N, r, a, x, out4);
+    residual_finalize_kernel<<<296, 256, 0, st>>>(seed, N, NB, P, myrow, mloc, r, a, x, out4);
     count_launch();
     return cudaGetLastError();
 }

@@ -104,7 +104,83 @@ laswp_gs_kernel(int jb, const int64_t *__restrict__ src, const int64_t *__restri
     }
 }
 
+// ---- P > 1: the row swaps cross process rows (RS over the column communicator)
+__device__ __forceinline__ bool owns_row(long long g, int NB, int P, int myrow)
+{
+    return (int)((g / NB) % P) == myrow;
+}
+__device__ __forceinline__ long long g2l_row(long long g, int NB, int P)
+{
+    return (g / ((long long)NB * P)) * NB + g % NB;
+}
+
+// U[k][c] = A[local(src[k])][c0 + c] when this process row owns src[k], else 0
+// (summed over the process column afterwards: every process gets all of U).
+__global__ void __launch_bounds__(LS_WARPS * 32)
+rs_pack_kernel(int jb, const int64_t *__restrict__ src, const double *__restrict__ A,
+               long long lda, long long c0, long long c1, double *U, long long ldu, int NB, int P,
+               int myrow)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long col = c0 + (long long)blockIdx.x * LS_COLS + 2 * lane;
+    const bool has0 = col < c1, has1 = col + 1 < c1;
+    for (int k = warp; k < jb; k += LS_WARPS) {
+        const long long g = src[k];
+        double *d = U + (long long)k * ldu + (col - c0);
+        if (owns_row(g, NB, P, myrow)) {
+            const double *sp = A + g2l_row(g, NB, P) * lda + col;
+            if (has0) d[0] = sp[0];
+            if (has1) d[1] = sp[1];
+        } else {
+            if (has0) d[0] = 0.0;
+            if (has1) d[1] = 0.0;
+        }
+    }
+}
+
+// A[local(d)][c0 + c] = W[s - j0][c] for the displaced pairs (d, s) this process row owns;
+// W holds the original block row j (broadcast from its owner).
+__global__ void __launch_bounds__(LS_WARPS * 32)
+rs_scatter_kernel(const int64_t *__restrict__ disp, const int *__restrict__ ndisp,
+                  const double *__restrict__ W, long long ldw, long long j0, double *A,
+                  long long lda, long long c0, long long c1, int NB, int P, int myrow)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long col = c0 + (long long)blockIdx.x * LS_COLS + 2 * lane;
+    const bool has0 = col < c1, has1 = col + 1 < c1;
+    const int nd = *ndisp;
+    for (int d = warp; d < nd; d += LS_WARPS) {
+        const long long g = disp[2 * d];
+        if (!owns_row(g, NB, P, myrow)) continue;
+        const double *sp = W + (disp[2 * d + 1] - j0) * ldw + (col - c0);
+        double *t = A + g2l_row(g, NB, P) * lda + col;
+        if (has0) t[0] = sp[0];
+        if (has1) t[1] = sp[1];
+    }
+}
+
 }  // namespace
+
+cudaError_t rs_pack(cudaStream_t st, int64_t jb, const int64_t *src, const double *A, int64_t lda,
+                    int64_t c0, int64_t c1, double *U, int64_t ldu, int NB, int P, int myrow)
+{
+    if (jb <= 0 || c1 <= c0) return cudaSuccess;
+    rs_pack_kernel<<<(unsigned)cdiv(c1 - c0, LS_COLS), LS_WARPS * 32, 0, st>>>(
+        (int)jb, src, A, lda, c0, c1, U, ldu, NB, P, myrow);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, const double *W,
+                       int64_t ldw, int64_t j0, double *A, int64_t lda, int64_t c0, int64_t c1,
+                       int NB, int P, int myrow)
+{
+    if (c1 <= c0) return cudaSuccess;
+    rs_scatter_kernel<<<(unsigned)cdiv(c1 - c0, LS_COLS), LS_WARPS * 32, 0, st>>>(
+        disp, ndisp, W, ldw, j0, A, lda, c0, c1, NB, P, myrow);
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t pivot_plan(cudaStream_t st, int64_t jb, int64_t r0, const int64_t *ipiv_rel,
                        int64_t goff, int64_t *gpiv, int64_t *src, int64_t *disp, int *ndisp)

@@ -59,3 +59,28 @@ def test_1x4_vs_oracle():
         pytest.skip("needs 4 GPUs")
     out = _run(4, 4096, 256, 1, 4)
     assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
+
+
+@pytest.mark.parametrize("N,NB", [(1024, 64), (2048, 128), (4000, 128)])
+def test_2x1_vs_oracle(N, NB):
+    """P = 2: distributed pivot search over NVLink peer memory + RS over the
+    column communicator."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = _run(2, N, NB, 2, 1)
+    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
+
+
+def test_2x1_no_lookahead():
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = _run(2, 2048, 128, 2, 1, ("--la", "0"))
+    assert out["ipiv_equal"] and out["resid"] < 16
+
+
+@pytest.mark.parametrize("N,NB,P,Q", [(4096, 256, 2, 2), (3000, 128, 4, 1), (2048, 64, 2, 2)])
+def test_4gpu_grids_vs_oracle(N, NB, P, Q):
+    if _ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    out = _run(4, N, NB, P, Q)
+    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
