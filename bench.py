@@ -36,14 +36,20 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_DERIVED = 148 * 128 * 1965e6 / 1e12  # SMs x FP64 flop/clk x max SM clock (TFLOP/s)
 
 
-# weak scaling: ~137 GB of A per GPU on a 1 x Q grid
+# weak scaling: ~130-137 GB of A per GPU (BASELINE.json configs; 2 GPUs: SURVEY C2b)
 N_BY_GPUS = {1: 131072, 2: 185344, 4: 262144, 8: 360448}
+GRID_BY_GPUS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 
 
 def workload(a, world: int):
-    """(N, NB, P, Q) of this run: --size, else the weak-scaled default."""
+    """(N, NB, P, Q) of this run: --size/--grid, else BASELINE.json's config."""
     n = a.n if a.n > 0 else N_BY_GPUS.get(world, int(131072 * world ** 0.5) // 512 * 512)
-    return n, a.nb, 1, world
+    if a.grid:
+        P, Q = (int(v) for v in a.grid.lower().split("x"))
+    else:
+        P, Q = GRID_BY_GPUS.get(world, (1, world))
+    assert P * Q == world, f"grid {P}x{Q} needs {P * Q} ranks, have {world}"
+    return n, a.nb, P, Q
 
 
 def hpl_flops(n: int) -> float:
@@ -58,6 +64,7 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--size", dest="n", type=int, default=0, help="HPL N (0 = weak-scaled default per GPU count)")
     ap.add_argument("--block", dest="nb", type=int, default=512)
+    ap.add_argument("--grid", default="", help="PxQ process grid (default: BASELINE.json's grid)")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--cpu-n", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
@@ -312,7 +319,9 @@ def main():
         "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
         "config": {"workload": f"HPL N={N} NB={NB} {P}x{Q} grid", "N": N, "NB": NB,
                    "grid": f"{P}x{Q}", "parallelism": "1 GPU" if world == 1 else
-                   f"2D block-cyclic {P}x{Q}, NCCL LBCAST along the process row",
+                   f"2D block-cyclic {P}x{Q}: NCCL LBCAST along process rows"
+                   + (", pivot exchange over NVLink peer memory + NCCL RS along process columns"
+                      if P > 1 else ""),
                    "lookahead": True, "l2": "inputs (~137 GB per GPU) >> L2, no flush needed",
                    "residual_max": max(resids), "frac_of_fp64_peak": value / world / FP64_PEAK_DERIVED},
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (trailing update)",
