@@ -84,3 +84,11 @@ def test_4gpu_grids_vs_oracle(N, NB, P, Q):
         pytest.skip("needs 4 GPUs")
     out = _run(4, N, NB, P, Q)
     assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
+
+
+@pytest.mark.parametrize("N,NB,P,Q", [(4096, 256, 2, 4), (4096, 128, 1, 8), (2500, 64, 4, 2)])
+def test_8gpu_grids_vs_oracle(N, NB, P, Q):
+    if _ngpu() < 8:
+        pytest.skip("needs 8 GPUs")
+    out = _run(8, N, NB, P, Q)
+    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
