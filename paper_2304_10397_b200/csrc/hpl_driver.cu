@@ -66,9 +66,13 @@ struct hpl_ctx {
     FactWork fw{};
     cudaStream_t s_la = nullptr, s_tr = nullptr;
     cudaEvent_t ev_panel[2] = {nullptr, nullptr}, ev_rest = nullptr;
+    cudaEvent_t ev_trsm = nullptr;   // rest(j)'s LASWP+DTRSM done: FACT(j+1) may start
     // options
     bool lookahead = true;
     int nbmin = 16;
+    bool leaf_auto = true;           // adaptive leaf grid (fact_panel)
+    int leaf_few_ctas = 8;
+    double leaf_hide_ms = 60.0;
     bool timing = false;
     std::vector<cudaEvent_t> tev;   // 7 events per iteration when timing
     std::vector<double> timeline;   // 6 values per iteration (ms)
@@ -202,6 +206,15 @@ hpl_status lbcast_and_plan(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 // FACT(j) (owner column) + LBCAST(j) + plan (everyone).
 hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 {
+    if (c->leaf_auto) {
+        // The leaf is latency-bound.  While a long trailing DGEMM runs beside it
+        // (FACT hidden), a few CTAs leave the SMs to the DGEMM; once the
+        // concurrent update is short (FACT on the critical path), use them all.
+        const int64_t j0 = j * c->NB, rows = c->mloc - lrows_before(c, j0);
+        const int64_t ncols = c->nloc - lcols_before(c, j0);
+        const double rest_ms = 2.0 * (double)rows * (double)ncols * c->NB / 35e12 * 1e3;
+        fact_set_leaf_ctas(rest_ms > c->leaf_hide_ms ? c->leaf_few_ctas : 0, 512);
+    }
     if (c->mycol == (int)(j % c->Q)) {
         hpl_status s = fact_local(c, st, j, b);
         if (s != HPL_OK) return s;
@@ -216,7 +229,7 @@ inline int64_t ucol(int64_t c) { return c + (c & 1); }
 // UPDATE(j) of local columns [c0, c1): LASWP, DTRSM (as L11^{-1} * U), DGEMM.
 // ev (optional, 4 events): recorded before LASWP, before DTRSM, before DGEMM, after.
 hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1,
-                       cudaEvent_t *ev = nullptr)
+                       cudaEvent_t *ev = nullptr, cudaEvent_t ev_pre_gemm = nullptr)
 {
     if (ev) CK(c, cudaEventRecord(ev[0], st));
     const int slot = st == c->s_la ? SLOT_LOOKAHEAD : SLOT_TRAIL;
@@ -262,6 +275,7 @@ hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0
                         c->ldu, -1, nullptr, 0, slot));
     }
     if (ev) CK(c, cudaEventRecord(ev[2], st));
+    if (ev_pre_gemm) CK(c, cudaEventRecord(ev_pre_gemm, st));
     const int64_t mrest = c->mloc - lrL0;
     if (mrest > 0 && n > 0)
         CK(c, dgemm(st, GEMM_UPDATE, false, mrest, n, jb, c->panel[b] + jb, ldpj, u2, c->ldu,
@@ -346,6 +360,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     CK(c, cudaStreamCreateWithPriority(&c->s_tr, cudaStreamNonBlocking, lo));
     for (int b = 0; b < 2; ++b) CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_trsm, cudaEventDisableTiming));
     for (int k = 0; k < 3; ++k) CK(c, cudaEventCreate(&c->ev_t[k]));
     return HPL_OK;
 }
@@ -380,6 +395,7 @@ void release(hpl_ctx *c)
     if (c->world) ncclCommDestroy(c->world);
     fact_work_free(&c->fw);
     if (c->ev_rest) cudaEventDestroy(c->ev_rest);
+    if (c->ev_trsm) cudaEventDestroy(c->ev_trsm);
     for (auto e : c->tev) cudaEventDestroy(e);
     for (int k = 0; k < 3; ++k)
         if (c->ev_t[k]) cudaEventDestroy(c->ev_t[k]);
@@ -522,7 +538,7 @@ hpl_status hpl_factor(hpl_ctx *c)
         cudaEvent_t *E = c->timing ? &c->tev[7 * j] : nullptr;
         if (c->lookahead) {
             CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_panel[b], 0));
-            s = update_cols(c, c->s_tr, j, b, lrest, cend, E);
+            s = update_cols(c, c->s_tr, j, b, lrest, cend, E, c->ev_trsm);
             if (s != HPL_OK) return s;
             CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
             if (E) CK(c, cudaEventRecord(E[4], c->s_la));
@@ -531,6 +547,9 @@ hpl_status hpl_factor(hpl_ctx *c)
                 if (s != HPL_OK) return s;
             }
             if (E) CK(c, cudaEventRecord(E[5], c->s_la));
+            // FACT(j+1) competes for SMs: let the rest's LASWP + DTRSM (on the
+            // critical path of S_tr) finish first; FACT then overlaps the DGEMM.
+            if (has_next) CK(c, cudaStreamWaitEvent(c->s_la, c->ev_trsm, 0));
             if (has_next) {
                 s = fact_panel(c, c->s_la, j + 1, b ^ 1);
                 if (s != HPL_OK) return s;
@@ -748,6 +767,10 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
         if (value < 1 || value > 16) return HPL_ERR_ARG;
         c->nbmin = (int)value;
     } else if (!strcmp(name, "gemm_cfg")) dgemm_set_default_cfg((int)value);
+    else if (!strcmp(name, "leaf_ctas")) { c->leaf_auto = false; fact_set_leaf_ctas((int)value, 0); }
+    else if (!strcmp(name, "leaf_rows")) { c->leaf_auto = false; fact_set_leaf_ctas(-1, (int)value); }
+    else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }
+    else if (!strcmp(name, "leaf_hide_ms")) { c->leaf_auto = true; c->leaf_hide_ms = (double)value; }
     else return HPL_ERR_ARG;
     return HPL_OK;
 }

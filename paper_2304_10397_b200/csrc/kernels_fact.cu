@@ -61,7 +61,38 @@ __device__ __forceinline__ void warp_argmax(double &v, long long &r)
     }
 }
 
+// Row update shared by both leaves: for panel row i, l = P[kc][i] / piv and
+// P[k0+cc][i] -= l * prow[cc] for the leaf columns cc > kk.  All the row's
+// loads are issued before any store (one L2 round trip instead of one per
+// column); returns the new |P[kc+1][i]| for the next column's pivot search.
+__device__ __forceinline__ double leaf_row_update(double *P, int64_t ldp, int k0, int w, int kk,
+                                                  int64_t i, double piv, const double *prow)
+{
+    const int kc = k0 + kk;
+    const double xk = P[(int64_t)kc * ldp + i];
+    double v[LEAF_MAX];
+#pragma unroll
+    for (int c = 0; c < LEAF_MAX; ++c) {
+        const int cc = kk + 1 + c;
+        v[c] = cc < w ? P[(int64_t)(k0 + cc) * ldp + i] : 0.0;
+    }
+    const double l = xk / piv;
+    P[(int64_t)kc * ldp + i] = l;
+#pragma unroll
+    for (int c = 0; c < LEAF_MAX; ++c) {
+        const int cc = kk + 1 + c;
+        if (cc < w) {
+            v[c] = fma(-l, prow[cc], v[c]);
+            P[(int64_t)(k0 + cc) * ldp + i] = v[c];
+        }
+    }
+    return fabs(v[0]);
+}
+
 // Leaf: right-looking GEPP of columns [k0, k0+w) of the panel (rows k0..m-1).
+// One grid barrier per column; the next column's local pivot candidate is
+// formed during the current column's update, so a column costs the barrier
+// plus about three L2 round trips.
 __global__ void __launch_bounds__(FACT_THREADS)
 leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, double *cand,
                  unsigned *bar, unsigned long long *info, long long goff)
@@ -73,21 +104,22 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
     const int rend = min(m, rbeg + chunk);
     __shared__ double s_v[FACT_THREADS / 32];
     __shared__ long long s_r[FACT_THREADS / 32];
+    __shared__ int s_c[FACT_THREADS / 32];
     __shared__ double s_prow[LEAF_MAX], s_rowk[LEAF_MAX];
     __shared__ long long s_p;
     __shared__ double s_piv;
 
+    // local candidate for the first leaf column
+    double bv = -1.0;
+    long long br = LLONG_MAX;
+    for (int i = max(rbeg, k0) + threadIdx.x; i < rend; i += FACT_THREADS) {
+        const double v = fabs(P[(int64_t)k0 * ldp + i]);
+        if (better(v, i, bv, br)) { bv = v; br = i; }
+    }
     for (int kk = 0; kk < w; ++kk) {
         const int kc = k0 + kk;
         double *rec = cand + (size_t)(kk & 1) * (MAX_CTAS + 1) * REC;
-        // ---- 1. local candidate over own rows >= kc
-        double bv = -1.0;
-        long long br = LLONG_MAX;
-        const double *colk = P + (int64_t)kc * ldp;
-        for (int i = max(rbeg, kc) + threadIdx.x; i < rend; i += FACT_THREADS) {
-            const double v = fabs(colk[i]);
-            if (better(v, i, bv, br)) { bv = v; br = i; }
-        }
+        // ---- 1. this CTA's candidate: (|v|, row, the row's leaf values)
         warp_argmax(bv, br);
         if ((threadIdx.x & 31) == 0) { s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; }
         __syncthreads();
@@ -118,8 +150,22 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
             const long long r = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
             if (r != LLONG_MAX && better(v, r, bv, br)) { bv = v; br = r; bc = c; }
         }
-        {
-            // argmax carrying the candidate index
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; s_c[threadIdx.x >> 5] = bc;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const bool ok = threadIdx.x < FACT_THREADS / 32;
+            bv = ok ? s_v[threadIdx.x] : -1.0;
+            br = ok ? s_r[threadIdx.x] : LLONG_MAX;
+            bc = ok ? s_c[threadIdx.x] : -1;
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -127,38 +173,21 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
                 const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
                 if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
             }
-            __shared__ int s_c[FACT_THREADS / 32];
-            if ((threadIdx.x & 31) == 0) {
-                s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; s_c[threadIdx.x >> 5] = bc;
+            if (threadIdx.x == 0) {
+                s_p = br;
+                s_piv = __ldcg(rec + (size_t)bc * REC + 2 + kk);
             }
-            __syncthreads();
-            if (threadIdx.x < 32) {
-                const bool ok = threadIdx.x < FACT_THREADS / 32;
-                bv = ok ? s_v[threadIdx.x] : -1.0;
-                br = ok ? s_r[threadIdx.x] : LLONG_MAX;
-                bc = ok ? s_c[threadIdx.x] : -1;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                    const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
-                    const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-                    if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
-                }
-                if (threadIdx.x == 0) s_p = br;
-                if (threadIdx.x < w) {
-                    s_prow[threadIdx.x] = __ldcg(rec + (size_t)bc * REC + 2 + threadIdx.x);
-                    s_rowk[threadIdx.x] = __ldcg(rec + (size_t)G * REC + 2 + threadIdx.x);
-                }
+            if (threadIdx.x < w) {
+                s_prow[threadIdx.x] = __ldcg(rec + (size_t)bc * REC + 2 + threadIdx.x);
+                s_rowk[threadIdx.x] = __ldcg(rec + (size_t)G * REC + 2 + threadIdx.x);
             }
-            __syncthreads();
         }
+        __syncthreads();
         const long long p = s_p;
-        if (threadIdx.x == 0) {
-            s_piv = s_prow[kk];
-            if (blockIdx.x == 0) {
-                ipiv[kc] = p;
-                if (s_prow[kk] == 0.0) atomicMin(info, (unsigned long long)(goff + kc));
-            }
+        const double piv = s_piv;
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            ipiv[kc] = p;
+            if (piv == 0.0) atomicMin(info, (unsigned long long)(goff + kc));
         }
         // ---- 3. swap rows kc and p inside the leaf columns (owners only)
         if (p != kc) {
@@ -168,36 +197,65 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
                 P[(int64_t)(k0 + threadIdx.x) * ldp + p] = s_rowk[threadIdx.x];
         }
         __syncthreads();
-        // ---- 4. scale column kc and rank-1 update of the leaf columns (own rows > kc)
-        const double piv = s_piv;
+        // ---- 4. scale + rank-1 update of own rows > kc; next column's candidate
+        bv = -1.0;
+        br = LLONG_MAX;
         for (int i = max(rbeg, kc + 1) + threadIdx.x; i < rend; i += FACT_THREADS) {
-            const double l = P[(int64_t)kc * ldp + i] / piv;
-            P[(int64_t)kc * ldp + i] = l;
-            for (int c = kk + 1; c < w; ++c) {
-                double *q = P + (int64_t)(k0 + c) * ldp + i;
-                *q = fma(-l, s_prow[c], *q);
-            }
+            const double nv = leaf_row_update(P, ldp, k0, w, kk, i, piv, s_prow);
+            if (kk + 1 < w && better(nv, i, bv, br)) { bv = nv; br = i; }
         }
-        __syncthreads();
     }
 }
 
 // Apply the leaf's swaps (ipiv[k0..k0+w), panel-relative) to the panel columns
-// outside the leaf: one thread per column, swaps in order (dlaswp semantics).
+// outside the leaf, dlaswp semantics.  Thread 0 turns the <= 16 sequential
+// swaps into "row r receives the old content of row s" moves (as pivot_plan
+// does for the trailing matrix); each thread then moves its column's rows
+// with all loads issued before the stores.
 __global__ void panel_laswp_kernel(int nb, int64_t ldp, double *P, int k0, int w,
                                    const int64_t *ipiv)
 {
+    __shared__ long long s_dst[2 * LEAF_MAX], s_src[2 * LEAF_MAX];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) {
+        long long topc[LEAF_MAX], lowr[LEAF_MAX], lowc[LEAF_MAX];
+        int nlow = 0;
+        for (int t = 0; t < w; ++t) topc[t] = k0 + t;
+        for (int t = 0; t < w; ++t) {
+            const long long pp = ipiv[k0 + t];
+            if (pp == k0 + t) continue;
+            if (pp < k0 + w) {
+                const long long tmp = topc[t];
+                topc[t] = topc[pp - k0];
+                topc[pp - k0] = tmp;
+            } else {
+                int f = -1;
+                for (int q = 0; q < nlow; ++q)
+                    if (lowr[q] == pp) f = q;
+                const long long content = f >= 0 ? lowc[f] : pp;
+                if (f >= 0) lowc[f] = topc[t];
+                else { lowr[nlow] = pp; lowc[nlow] = topc[t]; ++nlow; }
+                topc[t] = content;
+            }
+        }
+        int n = 0;
+        for (int t = 0; t < w; ++t)
+            if (topc[t] != k0 + t) { s_dst[n] = k0 + t; s_src[n] = topc[t]; ++n; }
+        for (int q = 0; q < nlow; ++q) { s_dst[n] = lowr[q]; s_src[n] = lowc[q]; ++n; }
+        s_n = n;
+    }
+    __syncthreads();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nb || (c >= k0 && c < k0 + w)) return;
     double *col = P + (int64_t)c * ldp;
-    for (int k = k0; k < k0 + w; ++k) {
-        const int64_t p = ipiv[k];
-        if (p != k) {
-            const double t = col[k];
-            col[k] = col[p];
-            col[p] = t;
-        }
-    }
+    const int n = s_n;
+    double v[2 * LEAF_MAX];
+#pragma unroll
+    for (int q = 0; q < 2 * LEAF_MAX; ++q)
+        if (q < n) v[q] = col[s_src[q]];
+#pragma unroll
+    for (int q = 0; q < 2 * LEAF_MAX; ++q)
+        if (q < n) col[s_dst[q]] = v[q];
 }
 
 // ---------------------------------------------------------------- P > 1 leaf
@@ -359,19 +417,15 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         }
         __syncthreads();
         // ---- 6. scale column kc and rank-1 update of the leaf columns (own rows > kc)
-        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += FACT_THREADS) {
-            const double l = Pn[(int64_t)kc * ldp + r] / piv;
-            Pn[(int64_t)kc * ldp + r] = l;
-            for (int c = kk + 1; c < w; ++c) {
-                double *q = Pn + (int64_t)(k0 + c) * ldp + r;
-                *q = fma(-l, s_pay[k0 + c], *q);
-            }
-        }
+        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += FACT_THREADS)
+            leaf_row_update(Pn, ldp, k0, w, kk, r, piv, s_pay + k0);
         __syncthreads();
     }
 }
 
 int g_num_sms = 0;
+int g_leaf_max_ctas = 0;        // 0 = all SMs
+int g_leaf_rows_per_cta = 512;
 
 cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
                         int64_t *ipiv, FactWork *wk, long long goff)
@@ -382,7 +436,8 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int 
         HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t rows = m - k0;
-    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, 512)), g_num_sms);
+    const int gmax = g_leaf_max_ctas > 0 ? std::min(g_leaf_max_ctas, g_num_sms) : g_num_sms;
+    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, g_leaf_rows_per_cta)), gmax);
     G = std::min(G, wk->max_ctas);
     int m_i = (int)m;
     int64_t ldp_ = ldp;
@@ -405,7 +460,8 @@ cudaError_t launch_leaf_dist(cudaStream_t st, int64_t m, double *P, int64_t ldp,
         HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     if (df->dp.jbp > 1024) return cudaErrorInvalidValue;
-    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(m, 512)), g_num_sms);
+    const int gmax = g_leaf_max_ctas > 0 ? std::min(g_leaf_max_ctas, g_num_sms) : g_num_sms;
+    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(m, g_leaf_rows_per_cta)), gmax);
     G = std::min(G, wk->max_ctas);
     int m_i = (int)m;
     int64_t ldp_ = ldp;
@@ -483,6 +539,12 @@ cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64
     maxloc_kernel<<<1, 32, 0, st>>>(n, absval, row, winner);
     count_launch();
     return cudaGetLastError();
+}
+
+void fact_set_leaf_ctas(int max_ctas, int rows_per_cta)
+{
+    if (max_ctas >= 0) g_leaf_max_ctas = max_ctas;
+    if (rows_per_cta > 0) g_leaf_rows_per_cta = rows_per_cta;
 }
 
 cudaError_t fact_work_alloc(FactWork *w)
