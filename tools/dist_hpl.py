@@ -39,6 +39,14 @@ def main():
     dist.broadcast(uid, 0)
     ctx = H.hpl_init_dist(N, NB, P, Q, seed, rank, world, bytes(uid.tolist()), local)
     H.hpl_set_option(ctx, "lookahead", la)
+    for kv in [a for a in sys.argv[1:] if a.startswith("--opt=")]:
+        k, v = kv[len("--opt="):].split("=")
+        H.hpl_set_option(ctx, k, int(v))
+    timeline = "--timeline" in sys.argv
+    if timeline:
+        H.hpl_set_timing(ctx, True)
+        H.hpl_factor(ctx)            # warm-up pass
+        H.hpl_regenerate(ctx)
     dist.barrier()
     t0 = time.perf_counter()
     H.hpl_factor(ctx)
@@ -46,6 +54,16 @@ def main():
     dist.barrier()
     wall = time.perf_counter() - t0
     tm = H.hpl_last_timing(ctx)
+    if timeline:
+        tl = H.hpl_get_timeline(ctx)
+        fact, la_, rest, lsw, trsm, dg = tl.T
+        summ = dict(rank=rank, factor_ms=round(tm["factor_ms"], 1), sum_fact=round(fact.sum(), 1),
+                    sum_la=round(la_.sum(), 1), sum_rest=round(rest.sum(), 1),
+                    sum_rs=round(lsw.sum(), 1), sum_trsm=round(trsm.sum(), 1),
+                    sum_dgemm=round(dg.sum(), 1),
+                    dgemm_tflops=round(tm["dgemm_flop"] / max(tm["dgemm_ms"], 1e-9) / 1e9, 2),
+                    fact_iter0=round(float(fact[0]), 2), rest_iter0=round(float(rest[0]), 2))
+        print(json.dumps(summ), flush=True)
     ipiv = H.hpl_get_ipiv(ctx)
     r = H.hpl_residual(ctx)
     H.hpl_free(ctx)
