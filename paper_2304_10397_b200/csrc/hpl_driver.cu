@@ -41,7 +41,7 @@ struct hpl_ctx {
     ncclComm_t col_comm_tr = nullptr;            // column comm used only by S_tr (RS of the rest)
     // P > 1: replicated top block, RS buffers (one set per stream), pivot exchange
     double *Tbuf = nullptr;
-    double *Ub[2] = {nullptr, nullptr}, *Wb[2] = {nullptr, nullptr};   // [0] = S_la, [1] = S_tr
+    double *Ub[3] = {nullptr, nullptr, nullptr}, *Wb[3] = {nullptr, nullptr, nullptr};  // la, right, left
     void *xbuf = nullptr;
     std::vector<void *> xpeer;
     DistExchange xch{};
@@ -67,6 +67,10 @@ struct hpl_ctx {
     cudaStream_t s_la = nullptr, s_tr = nullptr;
     cudaEvent_t ev_panel[2] = {nullptr, nullptr}, ev_rest = nullptr;
     cudaEvent_t ev_trsm = nullptr;   // rest(j)'s LASWP+DTRSM done: FACT(j+1) may start
+    // split update: RS of one section overlaps the UPDATE of the other
+    cudaStream_t s_rs = nullptr;
+    cudaEvent_t ev_rsR = nullptr, ev_rsL = nullptr, ev_dgR = nullptr, ev_dgL = nullptr;
+    int split_pct = -1;              // right-section share of the local columns; -1 = default
     // options
     bool lookahead = true;
     int nbmin = 16;
@@ -226,67 +230,100 @@ hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 // shifted by one when c is odd so every TMA operand starts 16-byte aligned.
 inline int64_t ucol(int64_t c) { return c + (c & 1); }
 
-// UPDATE(j) of local columns [c0, c1): LASWP, DTRSM (as L11^{-1} * U), DGEMM.
-// ev (optional, 4 events): recorded before LASWP, before DTRSM, before DGEMM, after.
-hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1,
-                       cudaEvent_t *ev = nullptr, cudaEvent_t ev_pre_gemm = nullptr)
+// Where the RS of a column range left the gathered block rows (U).
+struct RsOut {
+    double *u = nullptr;
+    int64_t ldu = 0;
+};
+enum { SEC_LA = 0, SEC_RIGHT = 1, SEC_LEFT = 2 };
+
+// RS(j) for local columns [c0, c1): the row interchanges of panel j.  P = 1:
+// one local gather/scatter pass; P > 1: across the process column (U = the
+// final block rows, each from its owner and summed with zeros elsewhere; W =
+// the original block row from its owner, for the displaced rows).
+hpl_status rs_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1, int sec,
+                   ncclComm_t comm, RsOut *out)
 {
-    if (ev) CK(c, cudaEventRecord(ev[0], st));
+    const int64_t j0 = j * c->NB, jb = jb_of(c, j), n = c1 - c0;
+    out->u = c->U + ucol(c0);
+    out->ldu = c->ldu;
+    if (n <= 0) return HPL_OK;
+    if (c->P == 1) {
+        CK(c, laswp_gather_scatter(st, jb, c->src[b], c->disp[b], c->ndisp[b], jb, c->A, c->lda,
+                                   c0, c1, out->u, c->ldu));
+        return HPL_OK;
+    }
+    const int64_t lr0 = lrows_before(c, j0);
+    const int64_t ldub = round_up(n, 16);
+    double *u = c->Ub[sec], *w = c->Wb[sec];
+    CK(c, rs_pack(st, jb, c->src[b], c->A, c->lda, c0, c1, u, ldub, c->NB, c->P, c->myrow));
+    if (c->myrow == prow_of(c, j))
+        CK(c, cudaMemcpy2DAsync(w, ldub * 8, c->A + lr0 * c->lda + c0, c->lda * 8, n * 8, jb,
+                                cudaMemcpyDeviceToDevice, st));
+    NK(c, ncclGroupStart());
+    NK(c, ncclAllReduce(u, u, (size_t)(jb * ldub), ncclDouble, ncclSum, comm, st));
+    NK(c, ncclBroadcast(w, w, (size_t)(jb * ldub), ncclDouble, prow_of(c, j), comm, st));
+    NK(c, ncclGroupEnd());
+    CK(c, rs_scatter(st, c->disp[b], c->ndisp[b], w, ldub, j0, c->A, c->lda, c0, c1, c->NB, c->P,
+                     c->myrow));
+    out->u = u;
+    out->ldu = ldub;
+    return HPL_OK;
+}
+
+// DTRSM + DGEMM(j) for local columns [c0, c1) once RS(j) has produced U.
+// ev_mid (optional) is recorded between the DTRSM and the DGEMM.
+hpl_status compute_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1,
+                        const RsOut &rs, cudaEvent_t ev_mid, bool count,
+                        cudaEvent_t ev_mid2 = nullptr)
+{
+    const int64_t n = c1 - c0;
+    if (n <= 0) {
+        if (ev_mid) CK(c, cudaEventRecord(ev_mid, st));
+        if (ev_mid2) CK(c, cudaEventRecord(ev_mid2, st));
+        return HPL_OK;
+    }
     const int slot = st == c->s_la ? SLOT_LOOKAHEAD : SLOT_TRAIL;
     const int64_t j0 = j * c->NB, jb = jb_of(c, j);
     const int64_t lr0 = lrows_before(c, j0), lrL0 = lrL0_of(c, j), ldpj = panel_ld(c, j);
-    const bool is_prow = c->myrow == prow_of(c, j);
-    const int64_t n = c1 - c0;
-    double *u = c->U + ucol(c0), *u2 = c->U2 + ucol(c0);
-    int64_t ldub = c->ldu;
-    double *top = c->A + lr0 * c->lda + c0;   // block row j (owner process row only)
-    if (n > 0 && c->P == 1) {
-        CK(c, laswp_gather_scatter(st, jb, c->src[b], c->disp[b], c->ndisp[b], jb, c->A, c->lda,
-                                   c0, c1, u, c->ldu));
-    } else if (n > 0) {
-        // RS across the process column: U = the final block rows (each row from
-        // its owner, summed with zeros elsewhere), W = the original block row
-        // (from its owner) for the displaced rows.
-        const int sidx = st == c->s_la ? 0 : 1;
-        ncclComm_t comm = st == c->s_la ? c->col_comm : c->col_comm_tr;
-        ldub = round_up(n, 16);
-        u = c->Ub[sidx];
-        double *w = c->Wb[sidx];
-        CK(c, rs_pack(st, jb, c->src[b], c->A, c->lda, c0, c1, u, ldub, c->NB, c->P, c->myrow));
-        if (is_prow)
-            CK(c, cudaMemcpy2DAsync(w, ldub * 8, top, c->lda * 8, n * 8, jb,
-                                    cudaMemcpyDeviceToDevice, st));
-        NK(c, ncclGroupStart());
-        NK(c, ncclAllReduce(u, u, (size_t)(jb * ldub), ncclDouble, ncclSum, comm, st));
-        NK(c, ncclBroadcast(w, w, (size_t)(jb * ldub), ncclDouble, prow_of(c, j), comm, st));
-        NK(c, ncclGroupEnd());
-        CK(c, rs_scatter(st, c->disp[b], c->ndisp[b], w, ldub, j0, c->A, c->lda, c0, c1, c->NB,
-                         c->P, c->myrow));
-    }
-    if (ev) CK(c, cudaEventRecord(ev[1], st));
+    double *u2 = c->U2 + ucol(c0);
     // block row j <- L11^{-1} U: into U2 (the DGEMM operand) and, on the owner
     // of block row j, into A as well
-    if (n > 0) {
-        if (is_prow)
-            CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, u, ldub, top,
-                        c->lda, -1, u2, c->ldu, slot));
-        else
-            CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, u, ldub, u2,
-                        c->ldu, -1, nullptr, 0, slot));
-    }
-    if (ev) CK(c, cudaEventRecord(ev[2], st));
-    if (ev_pre_gemm) CK(c, cudaEventRecord(ev_pre_gemm, st));
+    if (c->myrow == prow_of(c, j))
+        CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, rs.u, rs.ldu,
+                    c->A + lr0 * c->lda + c0, c->lda, -1, u2, c->ldu, slot));
+    else
+        CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, rs.u, rs.ldu, u2,
+                    c->ldu, -1, nullptr, 0, slot));
+    if (ev_mid) CK(c, cudaEventRecord(ev_mid, st));
+    if (ev_mid2) CK(c, cudaEventRecord(ev_mid2, st));
     const int64_t mrest = c->mloc - lrL0;
-    if (mrest > 0 && n > 0)
+    if (mrest > 0) {
         CK(c, dgemm(st, GEMM_UPDATE, false, mrest, n, jb, c->panel[b] + jb, ldpj, u2, c->ldu,
                     c->A + lrL0 * c->lda + c0, c->lda, -1, nullptr, 0, slot));
-    if (ev) {
-        CK(c, cudaEventRecord(ev[3], st));
-        if (mrest > 0 && n > 0) {
+        if (count) {
             c->dgemm_flop += 2.0 * (double)mrest * (double)n * (double)jb;
             c->dgemm_launches += 1;
         }
     }
+    return HPL_OK;
+}
+
+// UPDATE(j) of local columns [c0, c1) on one stream: RS, DTRSM, DGEMM.
+// ev (optional, 4 events): recorded before RS, before DTRSM, before DGEMM, after.
+hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1,
+                       cudaEvent_t *ev = nullptr, cudaEvent_t ev_pre_gemm = nullptr)
+{
+    if (ev) CK(c, cudaEventRecord(ev[0], st));
+    RsOut rs;
+    const bool la = st == c->s_la;
+    hpl_status s = rs_cols(c, st, j, b, c0, c1, la ? SEC_LA : SEC_RIGHT,
+                           la ? c->col_comm : c->col_comm_tr, &rs);
+    if (s != HPL_OK) return s;
+    if (ev) CK(c, cudaEventRecord(ev[1], st));
+    s = compute_cols(c, st, j, b, c0, c1, rs, ev ? ev[2] : nullptr, ev != nullptr, ev_pre_gemm);
+    if (s != HPL_OK) return s;
+    if (ev) CK(c, cudaEventRecord(ev[3], st));
     return HPL_OK;
 }
 
@@ -348,7 +385,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     if (c->P > 1) {
         const size_t rs = sizeof(double) * NBs * (size_t)round_up(c->nloc, 16);
         if (!M((void **)&c->Tbuf, sizeof(double) * NBs * NBs)) return HPL_ERR_OOM;
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 3; ++k) {
             if (!M((void **)&c->Ub[k], rs)) return HPL_ERR_OOM;
             if (!M((void **)&c->Wb[k], rs)) return HPL_ERR_OOM;
         }
@@ -358,6 +395,9 @@ hpl_status alloc_ctx(hpl_ctx *c)
     CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(c, cudaStreamCreateWithPriority(&c->s_la, cudaStreamNonBlocking, hi));
     CK(c, cudaStreamCreateWithPriority(&c->s_tr, cudaStreamNonBlocking, lo));
+    CK(c, cudaStreamCreateWithPriority(&c->s_rs, cudaStreamNonBlocking, hi));
+    for (cudaEvent_t *e : {&c->ev_rsR, &c->ev_rsL, &c->ev_dgR, &c->ev_dgL})
+        CK(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_trsm, cudaEventDisableTiming));
@@ -386,7 +426,7 @@ void release(hpl_ctx *c)
     cudaFree(c->gpiv); cudaFree(c->U); cudaFree(c->U2); cudaFree(c->scratch);
     cudaFree(c->x); cudaFree(c->tbuf); cudaFree(c->out4); cudaFree(c->rvec); cudaFree(c->avec);
     cudaFree(c->Tbuf);
-    for (int k = 0; k < 2; ++k) { cudaFree(c->Ub[k]); cudaFree(c->Wb[k]); }
+    for (int k = 0; k < 3; ++k) { cudaFree(c->Ub[k]); cudaFree(c->Wb[k]); }
     for (void *pp : c->xpeer) if (pp) cudaIpcCloseMemHandle(pp);
     cudaFree(c->xbuf);
     if (c->col_comm_tr) ncclCommDestroy(c->col_comm_tr);
@@ -396,6 +436,9 @@ void release(hpl_ctx *c)
     fact_work_free(&c->fw);
     if (c->ev_rest) cudaEventDestroy(c->ev_rest);
     if (c->ev_trsm) cudaEventDestroy(c->ev_trsm);
+    for (cudaEvent_t e : {c->ev_rsR, c->ev_rsL, c->ev_dgR, c->ev_dgL})
+        if (e) cudaEventDestroy(e);
+    if (c->s_rs) cudaStreamDestroy(c->s_rs);
     for (auto e : c->tev) cudaEventDestroy(e);
     for (int k = 0; k < 3; ++k)
         if (c->ev_t[k]) cudaEventDestroy(c->ev_t[k]);
@@ -526,6 +569,20 @@ hpl_status hpl_factor(hpl_ctx *c)
     hpl_status s = fact_panel(c, c->s_la, 0, 0);
     if (s != HPL_OK) return s;
     CK(c, cudaEventRecord(c->ev_panel[0], c->s_la));
+    // split update (option "split" = right-section percent; the paper uses 50 %,
+    // PAPER.md l.66).  Default off: on B200 the RS runs as SM-driven NCCL
+    // kernels over NVLink, so overlapping it with the DGEMM costs about as much
+    // DGEMM throughput as it hides.
+    const int split_pct = c->split_pct >= 0 ? c->split_pct : 0;
+    const bool split = c->lookahead && split_pct > 0;
+    int64_t split_col = c->nloc;
+    if (split) {
+        const int64_t n2 = std::min<int64_t>(
+            c->nloc, round_up((int64_t)((double)c->nloc * split_pct / 100.0), c->NB));
+        split_col = c->nloc - n2;
+        CK(c, cudaEventRecord(c->ev_dgR, c->s_tr));
+        CK(c, cudaEventRecord(c->ev_dgL, c->s_tr));
+    }
     for (int64_t j = 0; j < nblk; ++j) {
         const int b = (int)(j & 1);
         const int64_t j0 = j * c->NB, jb = jb_of(c, j);
@@ -536,11 +593,43 @@ hpl_status hpl_factor(hpl_ctx *c)
         const bool own_next = has_next && c->mycol == (int)((j + 1) % c->Q);
         const int64_t lrest = lct + (own_next ? jb1 : 0);
         cudaEvent_t *E = c->timing ? &c->tev[7 * j] : nullptr;
-        if (c->lookahead) {
+        if (c->lookahead && split) {
+            // Split update: right section [cs, cend) (fixed width n2, holds b) and
+            // left section [lrest, cs).  S_rs runs RS_R(j) then RS_L(j); S_tr runs
+            // UPDATE_R(j) then UPDATE_L(j).  RS_L(j) overlaps UPDATE_R(j) and
+            // RS_R(j+1) overlaps UPDATE_L(j).  Once the left section is used up the
+            // right section is the whole rest (the paper's fallback).
+            const int64_t cs = std::max(lrest, split_col);
+            RsOut rsR, rsL;
+            CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_panel[b], 0));
+            CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_dgR, 0));
+            if (E) CK(c, cudaEventRecord(E[0], c->s_rs));
+            s = rs_cols(c, c->s_rs, j, b, cs, cend, SEC_RIGHT, c->col_comm_tr, &rsR);
+            if (s != HPL_OK) return s;
+            CK(c, cudaEventRecord(c->ev_rsR, c->s_rs));
+            CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_dgL, 0));
+            s = rs_cols(c, c->s_rs, j, b, lrest, cs, SEC_LEFT, c->col_comm_tr, &rsL);
+            if (s != HPL_OK) return s;
+            CK(c, cudaEventRecord(c->ev_rsL, c->s_rs));
+            if (E) CK(c, cudaEventRecord(E[1], c->s_rs));
+            CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_rsR, 0));
+            s = compute_cols(c, c->s_tr, j, b, cs, cend, rsR, E ? E[2] : nullptr, E != nullptr,
+                             c->ev_trsm);
+            if (s != HPL_OK) return s;
+            CK(c, cudaEventRecord(c->ev_dgR, c->s_tr));
+            CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_rsL, 0));
+            s = compute_cols(c, c->s_tr, j, b, lrest, cs, rsL, nullptr, E != nullptr);
+            if (s != HPL_OK) return s;
+            CK(c, cudaEventRecord(c->ev_dgL, c->s_tr));
+            if (E) CK(c, cudaEventRecord(E[3], c->s_tr));
+            CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
+        } else if (c->lookahead) {
             CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_panel[b], 0));
             s = update_cols(c, c->s_tr, j, b, lrest, cend, E, c->ev_trsm);
             if (s != HPL_OK) return s;
             CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
+        }
+        if (c->lookahead) {
             if (E) CK(c, cudaEventRecord(E[4], c->s_la));
             if (own_next) {
                 s = update_cols(c, c->s_la, j, b, lct, lct + jb1);
@@ -769,6 +858,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     } else if (!strcmp(name, "gemm_cfg")) dgemm_set_default_cfg((int)value);
     else if (!strcmp(name, "leaf_ctas")) { c->leaf_auto = false; fact_set_leaf_ctas((int)value, 0); }
     else if (!strcmp(name, "leaf_rows")) { c->leaf_auto = false; fact_set_leaf_ctas(-1, (int)value); }
+    else if (!strcmp(name, "split")) c->split_pct = (int)value;
     else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }
     else if (!strcmp(name, "leaf_hide_ms")) { c->leaf_auto = true; c->leaf_hide_ms = (double)value; }
     else return HPL_ERR_ARG;

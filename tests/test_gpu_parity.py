@@ -181,6 +181,18 @@ def test_lookahead_schedule_invariance(H):
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb)
 
 
+def test_split_update_single_gpu_invariance(H):
+    """The split update on one GPU: identical pivots and x."""
+    def run(split):
+        with H.hpl_init(2048, 128, 1, 1, 13) as ctx:
+            H.hpl_set_option(ctx, "split", split)
+            H.hpl_factor(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+    xa, pa, ra = run(0)
+    xb, pb, rb = run(50)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
+
+
 def test_hpl_c1_vs_oracle(H):
     """BASELINE.json configs[1]: N=8192 NB=256 1x1."""
     N, NB, seed = 8192, 256, 42

@@ -92,3 +92,13 @@ def test_8gpu_grids_vs_oracle(N, NB, P, Q):
         pytest.skip("needs 8 GPUs")
     out = _run(8, N, NB, P, Q)
     assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
+
+
+def test_split_update_schedule_invariance():
+    """split update on/off gives the identical pivot sequence
+    (P = 2, RS across GPUs; the split update is the default there)."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    a = _run(2, 3072, 128, 2, 1, ("--opt=split=0",))
+    b = _run(2, 3072, 128, 2, 1, ("--opt=split=30",))
+    assert a["ipiv_equal"] and b["ipiv_equal"] and a["resid"] < 16 and b["resid"] < 16
