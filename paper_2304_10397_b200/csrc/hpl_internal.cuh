@@ -48,6 +48,8 @@ cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n,
                   int64_t ldc, int cfg = -1, double *C2 = nullptr, int64_t ldc2 = 0,
                   int slot = SLOT_TRAIL);
 void dgemm_set_default_cfg(int cfg);
+// Tiles per CTA for large DGEMM grids (1 = one tile per CTA).
+void dgemm_set_tiles_per_cta(int t);
 int dgemm_get_default_cfg();
 
 // ---------------------------------------------------------------- TRSM helpers

@@ -182,6 +182,10 @@ int hplk_maxloc(int64_t n, const double *absval, const int64_t *row, int64_t *wi
 int hplk_dgemm_bench(int64_t m, int64_t n, int64_t k, int32_t cfg, int32_t reps, double *ms_out)
 {
     if (m < 1 || n < 1 || k < 1 || reps < 1 || !ms_out) return -1;
+    if (cfg >= 100) {   // cfg = 100 * tiles_per_cta + tile config (measurement only)
+        dgemm_set_tiles_per_cta(cfg / 100);
+        cfg %= 100;
+    }
     const int64_t lda = round_up(m, 16), ldb = round_up(n, 16), ldc = ldb;
     Dev dA, dB, dC;
     KT(dA.alloc(sizeof(double) * lda * k));

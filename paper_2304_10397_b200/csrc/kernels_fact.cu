@@ -269,6 +269,16 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // Leaf of the distributed panel: as leaf_fact_kernel, but the candidate search
 // spans the process column.  Per column: local candidates -> grid barrier ->
@@ -280,8 +290,9 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 // identically by each, so only the winner's payload crosses NVLink.
 __global__ void __launch_bounds__(FACT_THREADS)
 leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ipiv, double *cand,
-                      double *win, double *tsnap, unsigned *bar, unsigned long long *info,
-                      DistPanel dp, DistExchange ex, unsigned long long seq0)
+                      double *win, double *tsnap, unsigned long long *winflag, unsigned *bar,
+                      unsigned long long *info, DistPanel dp, DistExchange ex,
+                      unsigned long long seq0)
 {
     const unsigned G = gridDim.x;
     const int chunk = (m + (int)G - 1) / (int)G;
@@ -336,40 +347,47 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         __threadfence();
         grid_barrier(bar, G);
 
-        // ---- 3. CTA 0: process-column exchange
+        // ---- 3. CTA 0: process-column exchange.  The other CTAs wait on the
+        // local "winner ready" flag instead of a second grid barrier.
         if (blockIdx.x == 0) {
-            if (threadIdx.x == 0) {
+            if (threadIdx.x < 32) {
                 bv = -1.0; bg = LLONG_MAX; br = -1;
-                for (unsigned c = 0; c < G; ++c) {
+                for (unsigned c = threadIdx.x; c < G; c += 32) {
                     const double v = __ldcg(rec + (size_t)c * REC);
                     const long long g = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
-                    if (g != LLONG_MAX && better(v, g, bv, bg)) {
-                        bv = v; bg = g;
-                        br = (int)__double_as_longlong(__ldcg(rec + (size_t)c * REC + 2));
-                    }
+                    const int r = (int)__double_as_longlong(__ldcg(rec + (size_t)c * REC + 2));
+                    if (g != LLONG_MAX && better(v, g, bv, bg)) { bv = v; bg = g; br = r; }
                 }
-                s_v[0] = bv; s_g[0] = bg; s_r[0] = br;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const long long og = __shfl_xor_sync(0xffffffffu, bg, o);
+                    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+                    if (better(ov, og, bv, bg)) { bv = ov; bg = og; br = orr; }
+                }
+                if (threadIdx.x == 0) { s_v[0] = bv; s_g[0] = bg; s_r[0] = br; }
             }
             __syncthreads();
             bv = s_v[0]; bg = s_g[0]; br = s_r[0];
             const size_t slot = ((size_t)par * ex.P + ex.myrow) * ex.recd;
-            for (int p = 0; p < ex.P; ++p) {
-                double *dst = ex.rec[p] + slot;
-                for (int c = threadIdx.x; c < jbp; c += FACT_THREADS)
-                    dst[2 + c] = br >= 0 ? __ldcg(Pn + (int64_t)c * ldp + br) : 0.0;
-                if (threadIdx.x == 0) {
-                    dst[0] = bv;
-                    dst[1] = __longlong_as_double(bg);
-                }
-            }
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS)
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+                const double pv = br >= 0 ? __ldcg(Pn + (int64_t)c * ldp + br) : 0.0;
+                for (int p = 0; p < ex.P; ++p) ex.rec[p][slot + 2 + c] = pv;
                 tsnap[c] = __ldcg(Pn + (int64_t)c * ldp + kc);
-            __threadfence_system();
+            }
+            if (threadIdx.x == 0)
+                for (int p = 0; p < ex.P; ++p) {
+                    ex.rec[p][slot] = bv;
+                    ex.rec[p][slot + 1] = __longlong_as_double(bg);
+                }
+            // bar.sync orders every thread's payload stores before the
+            // system-scope release of the flag (cumulativity)
             __syncthreads();
-            if (threadIdx.x < ex.P) st_release_sys(ex.flag[threadIdx.x] + (size_t)par * ex.P + ex.myrow, seq);
-            if (threadIdx.x < ex.P)
+            if (threadIdx.x < ex.P) {
+                st_release_sys(ex.flag[threadIdx.x] + (size_t)par * ex.P + ex.myrow, seq);
                 while (ld_acquire_sys(ex.my_flag + (size_t)par * ex.P + threadIdx.x) != seq) {
                 }
+            }
             __syncthreads();
             if (threadIdx.x == 0) {
                 int wslot = -1;
@@ -381,22 +399,36 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
                     if (g != LLONG_MAX && better(v, g, bv, bg)) { bv = v; bg = g; wslot = p; }
                 }
                 s_r[0] = wslot;
+                s_win = bg;
                 win[0] = __longlong_as_double(bg);
             }
             __syncthreads();
             const double *wr = ex.my_rec + ((size_t)par * ex.P + s_r[0]) * ex.recd;
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) win[2 + c] = __ldcv(wr + 2 + c);
-            __threadfence();
-        }
-        grid_barrier(bar, G);
-
-        // ---- 5. full-width swap on the owners of the two rows
-        if (threadIdx.x == 0) s_win = __double_as_longlong(__ldcg(win));
-        for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
-            s_pay[c] = __ldcg(win + 2 + c);
-            s_ts[c] = __ldcg(tsnap + c);
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+                const double v = __ldcv(wr + 2 + c);
+                win[2 + c] = v;
+                s_pay[c] = v;
+                s_ts[c] = tsnap[c];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                st_release_gpu(winflag, seq);
+            }
+        } else {
+            if (threadIdx.x == 0)
+                while (ld_acquire_gpu(winflag) != seq) {
+                }
+            __syncthreads();
+            if (threadIdx.x == 0) s_win = __double_as_longlong(__ldcg(win));
+            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+                s_pay[c] = __ldcg(win + 2 + c);
+                s_ts[c] = __ldcg(tsnap + c);
+            }
         }
         __syncthreads();
+
+        // ---- 5. full-width swap on the owners of the two rows
         const long long gw = s_win;
         const long long t = gw - dp.j0;
         if (kc >= rbeg && kc < rend)
@@ -468,8 +500,9 @@ cudaError_t launch_leaf_dist(cudaStream_t st, int64_t m, double *P, int64_t ldp,
     int k0_ = k0, w_ = w;
     unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
     unsigned long long seq0 = *df->seq;
+    unsigned long long *winflag = reinterpret_cast<unsigned long long *>(wk->bar + 8);
     void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->win, &wk->tsnap,
-                    &wk->bar, &info, &df->dp, &df->ex, &seq0};
+                    &winflag, &wk->bar, &info, &df->dp, &df->ex, &seq0};
     HPL_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)leaf_fact_dist_kernel, dim3(G),
                                              dim3(FACT_THREADS), args, 0, st));
     *df->seq += (unsigned long long)w;

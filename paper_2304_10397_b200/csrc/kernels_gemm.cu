@@ -44,6 +44,8 @@ struct GemmParams {
     int tiles_m, tiles_n;
     int prefetch_c;
     unsigned zero;       // always 0; opaque to the compiler (see release below)
+    int ntiles;          // tiles_m * tiles_n; CTA b owns tiles b, b + gridDim.x, ...
+    int tiles_per_cta;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -149,19 +151,22 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
     uint64_t *empty = full + C::STAGES;
 
-    // ---- grouped rasterisation of the tile grid
-    const int pid = blockIdx.x;
-    const int group_sz = GROUP_M * p.tiles_n;
-    const int gid = pid / group_sz;
-    const int first_m = gid * GROUP_M;
-    const int gm = min(p.tiles_m - first_m, GROUP_M);
-    const int pm = first_m + (pid % group_sz) % gm;
-    const int pn = (pid % group_sz) / gm;
-    const int m0 = pm * C::BM, n0 = pn * C::BN;
-
-    int k_end = p.k;
-    if (p.a_lower) k_end = min(p.k, m0 + C::BM);
-    const int nk = (k_end + BK - 1) / BK;
+    // ---- grouped rasterisation of the tile grid; several tiles per CTA share
+    // one continuous TMA/mbarrier pipeline (the next tile's stages load while
+    // the consumers run the current tile's epilogue)
+    auto tile_coords = [&](int tile, int &m0, int &n0, int &nk) {
+        const int group_sz = GROUP_M * p.tiles_n;
+        const int gid = tile / group_sz;
+        const int first_m = gid * GROUP_M;
+        const int gm = min(p.tiles_m - first_m, GROUP_M);
+        const int pm = first_m + (tile % group_sz) % gm;
+        const int pn = (tile % group_sz) / gm;
+        m0 = pm * C::BM;
+        n0 = pn * C::BN;
+        int k_end = p.k;
+        if (p.a_lower) k_end = min(p.k, m0 + C::BM);
+        nk = (k_end + BK - 1) / BK;
+    };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -179,18 +184,23 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % C::STAGES;
-                if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) & 1) ^ 1);
-                unsigned char *sA = smem + s * C::STAGE_BYTES;
-                unsigned char *sB = sA + C::A_STAGE;
-                mbar_expect_tx(&full[s], C::STAGE_BYTES);
+            int it = 0;
+            for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+                int m0, n0, nk;
+                tile_coords(tile, m0, n0, nk);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % C::STAGES;
+                    if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+                    unsigned char *sA = smem + s * C::STAGE_BYTES;
+                    unsigned char *sB = sA + C::A_STAGE;
+                    mbar_expect_tx(&full[s], C::STAGE_BYTES);
 #pragma unroll
-                for (int i = 0; i < C::A_BOXES; ++i)
-                    tma_load_2d(sA + i * BOX_BYTES, &tmA, p.a_x0 + m0 + 16 * i, kb * BK, &full[s]);
+                    for (int i = 0; i < C::A_BOXES; ++i)
+                        tma_load_2d(sA + i * BOX_BYTES, &tmA, p.a_x0 + m0 + 16 * i, kb * BK, &full[s]);
 #pragma unroll
-                for (int i = 0; i < C::B_BOXES; ++i)
-                    tma_load_2d(sB + i * BOX_BYTES, &tmB, p.b_x0 + n0 + 16 * i, kb * BK, &full[s]);
+                    for (int i = 0; i < C::B_BOXES; ++i)
+                        tma_load_2d(sB + i * BOX_BYTES, &tmB, p.b_x0 + n0 + 16 * i, kb * BK, &full[s]);
+                }
             }
         }
         return;
@@ -199,6 +209,14 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     // ================= consumers =================
     const int wm = warp / C::NWN, wn = warp % C::NWN;
     const int g = lane >> 2, t = lane & 3;
+    const int a_box0 = (wm * C::WM) / 16;
+    const int b_box0 = (wn * C::WN) / 16;
+    const uint32_t smem_base = smem_u32(smem);
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && ((p.ldc & 1) == 0);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    int m0, n0, nk;
+    tile_coords(tile, m0, n0, nk);
     const int row_base = m0 + wm * C::WM;   // first row of this warp's tile
     const int col_base = n0 + wn * C::WN;
 
@@ -227,13 +245,9 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[i][j][h][c] = 0.0;
 
-    const int a_box0 = (wm * C::WM) / 16;
-    const int b_box0 = (wn * C::WN) / 16;
-
-    const uint32_t smem_base = smem_u32(smem);
-    for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        mbar_wait(&full[s], (kb / C::STAGES) & 1);
+    for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % C::STAGES;
+        mbar_wait(&full[s], (it / C::STAGES) & 1);
         // dep folds one word of every fragment loaded from this stage; the
         // release below uses it (masked by a runtime zero) in its address, so
         // the empty-barrier arrive cannot issue before every LDS of the stage
@@ -271,7 +285,6 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     }
 
     // ================= epilogue: C -= acc  (or C = acc) =================
-    const bool vec_ok = ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0) && ((p.ldc & 1) == 0);
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
 #pragma unroll
@@ -317,6 +330,7 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
             }
         }
     }
+    }  // tile loop
 }
 
 // ---------------------------------------------------------------- host side
@@ -366,6 +380,7 @@ using CfgC = Cfg<64, 64, 32, 32, 4, 3>;
 using CfgD = Cfg<64, 64, 32, 32, 6, 2>;
 
 int g_default_cfg = 2;
+int g_tiles_per_cta = 1;
 
 template <class C, int SLOT>
 cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
@@ -377,7 +392,7 @@ cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMa
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
-    const long long grid = (long long)p.tiles_m * p.tiles_n;
+    const long long grid = cdiv(p.ntiles, p.tiles_per_cta);
     ParamPad<SLOT> pad{};
     dgemm_tma_kernel<C, SLOT><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
     count_launch();
@@ -390,6 +405,10 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
 {
     p.tiles_m = (int)cdiv(p.m, C::BM);
     p.tiles_n = (int)cdiv(p.n, C::BN);
+    p.ntiles = p.tiles_m * p.tiles_n;
+    // several tiles per CTA only for large grids (short kernels keep one tile
+    // per CTA so concurrent FACT kernels find free SM slots quickly)
+    p.tiles_per_cta = p.ntiles >= 16 * 148 * C::MINB ? g_tiles_per_cta : 1;
     switch (slot) {
     case 1: return launch_slot<C, 1>(st, ma, mb, p);
     case 2: return launch_slot<C, 2>(st, ma, mb, p);
@@ -400,6 +419,7 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
 }  // namespace
 
 void dgemm_set_default_cfg(int cfg) { g_default_cfg = cfg; }
+void dgemm_set_tiles_per_cta(int t) { g_tiles_per_cta = t > 0 ? t : 1; }
 int dgemm_get_default_cfg() { return g_default_cfg; }
 
 cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n, int64_t k,
