@@ -50,13 +50,14 @@ struct hpl_ctx {
     // local storage
     int64_t mloc = 0, nloc = 0, lda = 0;
     double *A = nullptr;
-    double *panel[2] = {nullptr, nullptr};
+    static constexpr int NBUF = 3;   // per-panel state: panels j, j+1, j+2 live at once
+    double *panel[NBUF] = {};
     int64_t ldp = 0;
-    double *linv[2] = {nullptr, nullptr};
+    double *linv[NBUF] = {};
     int64_t ldlinv = 0;
-    int64_t *src[2] = {nullptr, nullptr};
-    int64_t *disp[2] = {nullptr, nullptr};
-    int *ndisp[2] = {nullptr, nullptr};
+    int64_t *src[NBUF] = {};
+    int64_t *disp[NBUF] = {};
+    int *ndisp[NBUF] = {};
     int64_t *gpiv = nullptr;
     double *U = nullptr;     // gathered block rows (pre-DTRSM), NB x ldu
     double *U2 = nullptr;    // L11^{-1} U (the DGEMM's B operand), NB x ldu
@@ -65,7 +66,8 @@ struct hpl_ctx {
     double *x = nullptr, *tbuf = nullptr, *out4 = nullptr;
     FactWork fw{};
     cudaStream_t s_la = nullptr, s_tr = nullptr;
-    cudaEvent_t ev_panel[2] = {nullptr, nullptr}, ev_rest = nullptr;
+    cudaEvent_t ev_panel[NBUF] = {}, ev_rest = nullptr;
+    cudaEvent_t ev_next = nullptr;   // rest(j) has updated panel j+2's columns
     cudaEvent_t ev_trsm = nullptr;   // rest(j)'s LASWP+DTRSM done: FACT(j+1) may start
     // split update: RS of one section overlaps the UPDATE of the other
     cudaStream_t s_rs = nullptr;
@@ -73,6 +75,8 @@ struct hpl_ctx {
     int split_pct = -1;              // right-section share of the local columns; -1 = default
     // options
     bool lookahead = true;
+    bool hp_trsm = true;             // rest RS + DTRSM on the high-priority stream
+    bool early_next = false;         // (option) update panel j+2's columns first inside rest(j)
     int nbmin = 16;
     bool leaf_auto = true;           // adaptive leaf grid (fact_panel)
     int leaf_few_ctas = 8;
@@ -275,7 +279,7 @@ hpl_status rs_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, in
 // ev_mid (optional) is recorded between the DTRSM and the DGEMM.
 hpl_status compute_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, int64_t c1,
                         const RsOut &rs, cudaEvent_t ev_mid, bool count,
-                        cudaEvent_t ev_mid2 = nullptr)
+                        cudaEvent_t ev_mid2 = nullptr, bool do_trsm = true, bool do_gemm = true)
 {
     const int64_t n = c1 - c0;
     if (n <= 0) {
@@ -289,16 +293,18 @@ hpl_status compute_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c
     double *u2 = c->U2 + ucol(c0);
     // block row j <- L11^{-1} U: into U2 (the DGEMM operand) and, on the owner
     // of block row j, into A as well
-    if (c->myrow == prow_of(c, j))
-        CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, rs.u, rs.ldu,
-                    c->A + lr0 * c->lda + c0, c->lda, -1, u2, c->ldu, slot));
-    else
-        CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, rs.u, rs.ldu, u2,
-                    c->ldu, -1, nullptr, 0, slot));
+    if (do_trsm) {
+        if (c->myrow == prow_of(c, j))
+            CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, rs.u, rs.ldu,
+                        c->A + lr0 * c->lda + c0, c->lda, -1, u2, c->ldu, slot));
+        else
+            CK(c, dgemm(st, GEMM_ASSIGN, true, jb, n, jb, c->linv[b], c->ldlinv, rs.u, rs.ldu, u2,
+                        c->ldu, -1, nullptr, 0, slot));
+    }
     if (ev_mid) CK(c, cudaEventRecord(ev_mid, st));
     if (ev_mid2) CK(c, cudaEventRecord(ev_mid2, st));
     const int64_t mrest = c->mloc - lrL0;
-    if (mrest > 0) {
+    if (mrest > 0 && do_gemm) {
         CK(c, dgemm(st, GEMM_UPDATE, false, mrest, n, jb, c->panel[b] + jb, ldpj, u2, c->ldu,
                     c->A + lrL0 * c->lda + c0, c->lda, -1, nullptr, 0, slot));
         if (count) {
@@ -365,7 +371,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     };
     const size_t NBs = (size_t)c->NB;
     if (!M((void **)&c->A, sizeof(double) * (size_t)c->mloc * c->lda)) return HPL_ERR_OOM;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < hpl_ctx::NBUF; ++b) {
         if (!M((void **)&c->panel[b], sizeof(double) * (size_t)c->ldp * (NBs + 1))) return HPL_ERR_OOM;
         if (!M((void **)&c->linv[b], sizeof(double) * (size_t)c->ldlinv * NBs)) return HPL_ERR_OOM;
         if (!M((void **)&c->src[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
@@ -398,7 +404,9 @@ hpl_status alloc_ctx(hpl_ctx *c)
     CK(c, cudaStreamCreateWithPriority(&c->s_rs, cudaStreamNonBlocking, hi));
     for (cudaEvent_t *e : {&c->ev_rsR, &c->ev_rsL, &c->ev_dgR, &c->ev_dgL})
         CK(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    for (int b = 0; b < 2; ++b) CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
+    for (int b = 0; b < hpl_ctx::NBUF; ++b)
+        CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_next, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_trsm, cudaEventDisableTiming));
     for (int k = 0; k < 3; ++k) CK(c, cudaEventCreate(&c->ev_t[k]));
@@ -418,10 +426,11 @@ void release(hpl_ctx *c)
 {
     if (!c) return;
     cudaFree(c->A);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < hpl_ctx::NBUF; ++b) {
         cudaFree(c->panel[b]); cudaFree(c->linv[b]); 
         cudaFree(c->src[b]); cudaFree(c->disp[b]); cudaFree(c->ndisp[b]);
         if (c->ev_panel[b]) cudaEventDestroy(c->ev_panel[b]);
+        if (b == 0 && c->ev_next) cudaEventDestroy(c->ev_next);
     }
     cudaFree(c->gpiv); cudaFree(c->U); cudaFree(c->U2); cudaFree(c->scratch);
     cudaFree(c->x); cudaFree(c->tbuf); cudaFree(c->out4); cudaFree(c->rvec); cudaFree(c->avec);
@@ -565,6 +574,8 @@ hpl_status hpl_factor(hpl_ctx *c)
     c->dgemm_launches = 0;
     CK(c, cudaEventRecord(c->ev_t[0], c->s_la));
     CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_t[0], 0));
+    CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_t[0], 0));
+    CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
     CK(c, cudaMemsetAsync(c->fw.info, 0xff, sizeof(int64_t), c->s_la));
     hpl_status s = fact_panel(c, c->s_la, 0, 0);
     if (s != HPL_OK) return s;
@@ -584,7 +595,7 @@ hpl_status hpl_factor(hpl_ctx *c)
         CK(c, cudaEventRecord(c->ev_dgL, c->s_tr));
     }
     for (int64_t j = 0; j < nblk; ++j) {
-        const int b = (int)(j & 1);
+        const int b = (int)(j % hpl_ctx::NBUF), bn = (int)((j + 1) % hpl_ctx::NBUF);
         const int64_t j0 = j * c->NB, jb = jb_of(c, j);
         const int64_t lct = lcols_before(c, j0 + jb), cend = c->nloc;  // local trailing cols
         const bool has_next = j + 1 < nblk;
@@ -623,10 +634,46 @@ hpl_status hpl_factor(hpl_ctx *c)
             CK(c, cudaEventRecord(c->ev_dgL, c->s_tr));
             if (E) CK(c, cudaEventRecord(E[3], c->s_tr));
             CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
+            CK(c, cudaEventRecord(c->ev_next, c->s_tr));
         } else if (c->lookahead) {
+            // Update panel j+2's columns (on their owner: the first rest columns)
+            // before the remainder, so la(j+1) and FACT(j+2) can start while the
+            // remainder of rest(j) runs: FACT(j+2) then hides behind the rest of
+            // iteration j and all of iteration j+1 (SURVEY §3.4 refinement).
             CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_panel[b], 0));
-            s = update_cols(c, c->s_tr, j, b, lrest, cend, E, c->ev_trsm);
-            if (s != HPL_OK) return s;
+            const bool has_next2 = j + 2 < nblk;
+            const int64_t jb2 = has_next2 ? jb_of(c, j + 2) : 0;
+            const bool own_next2 = has_next2 && c->mycol == (int)((j + 2) % c->Q);
+            if (c->early_next && own_next2 && lrest + jb2 < cend) {
+                s = update_cols(c, c->s_tr, j, b, lrest, lrest + jb2, nullptr, c->ev_trsm);
+                if (s != HPL_OK) return s;
+                CK(c, cudaEventRecord(c->ev_next, c->s_tr));
+                s = update_cols(c, c->s_tr, j, b, lrest + jb2, cend, E);
+                if (s != HPL_OK) return s;
+            } else if (c->hp_trsm) {
+                // RS + DTRSM of the rest on the high-priority S_rs (critical path),
+                // only the long DGEMM at low priority on S_tr
+                RsOut rs;
+                CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_panel[b], 0));
+                CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_rest, 0));
+                if (E) CK(c, cudaEventRecord(E[0], c->s_rs));
+                s = rs_cols(c, c->s_rs, j, b, lrest, cend, SEC_RIGHT, c->col_comm_tr, &rs);
+                if (s != HPL_OK) return s;
+                if (E) CK(c, cudaEventRecord(E[1], c->s_rs));
+                s = compute_cols(c, c->s_rs, j, b, lrest, cend, rs, E ? E[2] : nullptr, false,
+                                 c->ev_trsm, true, false);
+                if (s != HPL_OK) return s;
+                CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_trsm, 0));
+                s = compute_cols(c, c->s_tr, j, b, lrest, cend, rs, nullptr, E != nullptr, nullptr,
+                                 false, true);
+                if (s != HPL_OK) return s;
+                if (E) CK(c, cudaEventRecord(E[3], c->s_tr));
+                CK(c, cudaEventRecord(c->ev_next, c->s_tr));
+            } else {
+                s = update_cols(c, c->s_tr, j, b, lrest, cend, E, c->ev_trsm);
+                if (s != HPL_OK) return s;
+                CK(c, cudaEventRecord(c->ev_next, c->s_tr));
+            }
             CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
         }
         if (c->lookahead) {
@@ -640,19 +687,20 @@ hpl_status hpl_factor(hpl_ctx *c)
             // critical path of S_tr) finish first; FACT then overlaps the DGEMM.
             if (has_next) CK(c, cudaStreamWaitEvent(c->s_la, c->ev_trsm, 0));
             if (has_next) {
-                s = fact_panel(c, c->s_la, j + 1, b ^ 1);
+                s = fact_panel(c, c->s_la, j + 1, bn);
                 if (s != HPL_OK) return s;
-                CK(c, cudaEventRecord(c->ev_panel[b ^ 1], c->s_la));
+                CK(c, cudaEventRecord(c->ev_panel[bn], c->s_la));
             }
             if (E) CK(c, cudaEventRecord(E[6], c->s_la));
-            CK(c, cudaStreamWaitEvent(c->s_la, c->ev_rest, 0));
+            // la(j+1) touches panel j+2's columns: wait until rest(j) updated them
+            CK(c, cudaStreamWaitEvent(c->s_la, c->ev_next, 0));
         } else {
             if (E) CK(c, cudaEventRecord(E[4], c->s_la));
             s = update_cols(c, c->s_la, j, b, lct, cend, E);
             if (s != HPL_OK) return s;
             if (E) CK(c, cudaEventRecord(E[5], c->s_la));
             if (has_next) {
-                s = fact_panel(c, c->s_la, j + 1, b ^ 1);
+                s = fact_panel(c, c->s_la, j + 1, bn);
                 if (s != HPL_OK) return s;
             }
             if (E) CK(c, cudaEventRecord(E[6], c->s_la));
@@ -860,6 +908,8 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "leaf_ctas")) { c->leaf_auto = false; fact_set_leaf_ctas((int)value, 0); }
     else if (!strcmp(name, "leaf_rows")) { c->leaf_auto = false; fact_set_leaf_ctas(-1, (int)value); }
     else if (!strcmp(name, "split")) c->split_pct = (int)value;
+    else if (!strcmp(name, "early_next")) c->early_next = value != 0;
+    else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }
     else if (!strcmp(name, "leaf_hide_ms")) { c->leaf_auto = true; c->leaf_hide_ms = (double)value; }
     else return HPL_ERR_ARG;
