@@ -298,11 +298,14 @@ def main():
                "sample": f"oracle GEPP+solves, full solve at N={a.cpu_n} ({dt:.1f} s; bounded "
                          f"sample of the N={N} workload), {cpu_model()}", "resid": rr}
 
-    traffic = None
+    traffic, traffic_note = None, None
     tf_path = os.path.join(ROOT, "profiles", "dgemm_traffic.json")
     if os.path.exists(tf_path):
         try:
-            traffic = json.load(open(tf_path)).get("traffic_bytes_per_launch")
+            tj = json.load(open(tf_path))
+            traffic = tj.get("traffic_bytes_per_launch")
+            traffic_note = (f"dram read+write per launch at {tj.get('shape')}; algorithmic "
+                            f"{tj.get('algorithmic_bytes_per_launch')} B")
         except Exception:
             traffic = None
 
@@ -327,7 +330,8 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (trailing update)",
                      "achieved": dg_tf, "peak": FP64_PEAK_DERIVED, "unit": "TFLOP/s",
                      "frac": (dg_tf / FP64_PEAK_DERIVED) if dg_tf else None,
-                     "traffic": traffic, "launches": dg_n // max(1, a.steps),
+                     "traffic": traffic, "traffic_note": traffic_note,
+                     "launches": dg_n // max(1, a.steps),
                      "peak_source": "derived 148 SM x 128 FP64 flop/clk x 1965 MHz (MEASURED_PEAKS"
                                     ".json has no FP64 entry)",
                      "peak_measured_dmma": peak_meas},

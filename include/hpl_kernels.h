@@ -69,6 +69,13 @@ int hplk_maxloc(int64_t n, const double *absval, const int64_t *row, int64_t *wi
  * launching stream after one warm-up launch.  ms_out[r] = duration of launch r. */
 int hplk_dgemm_bench(int64_t m, int64_t n, int64_t k, int32_t cfg, int32_t reps, double *ms_out);
 
+/* Measurement hook (device analog of PAPER.md Fig. pfact-mptest): time the
+ * device panel FACT of an m x nb seeded panel, device-resident, `reps` times
+ * (fresh panel each time, CUDA events); leaf_ctas = leaf grid cap (0 = all
+ * SMs).  ms_out[r] = duration of rep r.  Returns -2 on a singular panel. */
+int hplk_panel_bench(int64_t m, int64_t nb, int32_t nbmin, int32_t leaf_ctas, int32_t reps,
+                     double *ms_out);
+
 /* Measurement hook: FP64 tensor-pipe ceiling.  Runs a register-resident chain
  * of mma.sync.m16n8k4.f64 (SASS DMMA) on blocks_per_sm CTAs of `warps` warps
  * per SM; out2 = {ms, flop}. */

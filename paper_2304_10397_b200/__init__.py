@@ -8,6 +8,6 @@ from .hpl import (  # noqa: F401
     hpl_get_timeline, hpl_get_unique_id, hpl_init, hpl_init_dist, hpl_last_timing,
     hpl_launch_count, hpl_pin_host, hpl_plan_iteration,
     hpl_load_local, hpl_regenerate, hpl_residual, hpl_set_option, hpl_set_timing,
-    hpl_solve, hplk_back_solve, hplk_dgemm_bench, hplk_dgemm_update, hplk_dmma_peak, hplk_generate, hplk_laswp,
+    hpl_solve, hplk_back_solve, hplk_dgemm_bench, hplk_dgemm_update, hplk_dmma_peak, hplk_panel_bench, hplk_generate, hplk_laswp,
     hplk_maxloc, hplk_panel_fact, hplk_trsm,
 )

@@ -67,6 +67,7 @@ _sig("hplk_generate", ctypes.c_int, [u64, i64, i64, i64, i64, i64, vp])
 _sig("hplk_maxloc", ctypes.c_int, [i64, vp, vp, ctypes.POINTER(i64)])
 _sig("hplk_dgemm_bench", ctypes.c_int, [i64, i64, i64, i32, i32, vp])
 _sig("hplk_dmma_peak", ctypes.c_int, [i32, i32, i32, vp])
+_sig("hplk_panel_bench", ctypes.c_int, [i64, i64, i32, i32, i32, vp])
 
 EXPORTED = [
     "hpl_init", "hpl_init_dist", "hpl_get_unique_id", "hpl_factor", "hpl_solve",
@@ -75,7 +76,7 @@ EXPORTED = [
     "hpl_get_timeline", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
     "hpl_last_timing", "hpl_plan_iteration", "hpl_pin_host",
     "hplk_dgemm_update", "hplk_trsm", "hplk_panel_fact", "hplk_laswp", "hplk_back_solve",
-    "hplk_generate", "hplk_maxloc", "hplk_dgemm_bench", "hplk_dmma_peak",
+    "hplk_generate", "hplk_maxloc", "hplk_dgemm_bench", "hplk_dmma_peak", "hplk_panel_bench",
 ]
 
 

@@ -905,6 +905,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
         c->nbmin = (int)value;
     } else if (!strcmp(name, "gemm_cfg")) dgemm_set_default_cfg((int)value);
     else if (!strcmp(name, "gemm_tpc")) dgemm_set_tiles_per_cta((int)value);
+    else if (!strcmp(name, "gemm_red")) dgemm_set_red_epilogue((int)value);
     else if (!strcmp(name, "leaf_ctas")) { c->leaf_auto = false; fact_set_leaf_ctas((int)value, 0); }
     else if (!strcmp(name, "leaf_rows")) { c->leaf_auto = false; fact_set_leaf_ctas(-1, (int)value); }
     else if (!strcmp(name, "split")) c->split_pct = (int)value;

@@ -50,6 +50,8 @@ cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n,
 void dgemm_set_default_cfg(int cfg);
 // Tiles per CTA for large DGEMM grids (1 = one tile per CTA).
 void dgemm_set_tiles_per_cta(int t);
+// UPDATE epilogue via red.global.add.f64 (no C load round trip); 0 = load/sub/store.
+void dgemm_set_red_epilogue(int on);
 int dgemm_get_default_cfg();
 
 // ---------------------------------------------------------------- TRSM helpers

@@ -182,8 +182,9 @@ int hplk_maxloc(int64_t n, const double *absval, const int64_t *row, int64_t *wi
 int hplk_dgemm_bench(int64_t m, int64_t n, int64_t k, int32_t cfg, int32_t reps, double *ms_out)
 {
     if (m < 1 || n < 1 || k < 1 || reps < 1 || !ms_out) return -1;
-    if (cfg >= 100) {   // cfg = 100 * tiles_per_cta + tile config (measurement only)
-        dgemm_set_tiles_per_cta(cfg / 100);
+    if (cfg >= 0) {     // cfg = 1000 * red_epilogue + 100 * tiles_per_cta + tile config
+        dgemm_set_red_epilogue(cfg / 1000);
+        dgemm_set_tiles_per_cta(std::max(1, (cfg % 1000) / 100));
         cfg %= 100;
     }
     const int64_t lda = round_up(m, 16), ldb = round_up(n, 16), ldc = ldb;
@@ -212,6 +213,43 @@ int hplk_dgemm_bench(int64_t m, int64_t n, int64_t k, int32_t cfg, int32_t reps,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return 0;
+}
+
+int hplk_panel_bench(int64_t m, int64_t nb, int32_t nbmin, int32_t leaf_ctas, int32_t reps,
+                     double *ms_out)
+{
+    if (m < nb || nb < 1 || nb > 1024 || nbmin < 1 || nbmin > 16 || reps < 1 || !ms_out) return -1;
+    const int64_t ldp = round_up(m, 16);
+    Dev dP, dI, dS;
+    FactWork fw{};
+    KT(dP.alloc(sizeof(double) * ldp * nb));
+    KT(dI.alloc(sizeof(int64_t) * nb));
+    KT(dS.alloc(sizeof(double) * round_up(nb, 16) * nb));
+    KT(fact_work_alloc(&fw));
+    fact_set_leaf_ctas(leaf_ctas, 512);
+    cudaEvent_t e0, e1;
+    KT(cudaEventCreate(&e0));
+    KT(cudaEventCreate(&e1));
+    int64_t inf = -1;
+    for (int r = -1; r < reps; ++r) {   // r = -1: warm-up
+        // column-major m x nb panel of the seeded HPL system (rows = panel rows)
+        KT(gen_local(0, 11 + r, std::max(m, nb) + 1, 1 << 20, 1, 1, 0, 0, nb, ldp, dP.as<double>(),
+                     ldp));
+        KT(cudaEventRecord(e0, 0));
+        KT(panel_fact(0, m, nb, dP.as<double>(), ldp, dI.as<int64_t>(), nbmin, &fw,
+                      dS.as<double>(), 0));
+        KT(cudaEventRecord(e1, 0));
+        KT(cudaEventSynchronize(e1));
+        float t = 0;
+        KT(cudaEventElapsedTime(&t, e0, e1));
+        if (r >= 0) ms_out[r] = t;
+    }
+    KT(cudaMemcpy(&inf, fw.info, sizeof inf, cudaMemcpyDeviceToHost));
+    fact_set_leaf_ctas(0, 512);
+    fact_work_free(&fw);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return inf == -1 ? 0 : -2;
 }
 
 int hplk_dmma_peak(int32_t iters, int32_t blocks_per_sm, int32_t warps, double *out2)

@@ -44,6 +44,7 @@ struct GemmParams {
     int tiles_m, tiles_n;
     int prefetch_c;
     unsigned zero;       // always 0; opaque to the compiler (see release below)
+    int red_epi;         // UPDATE epilogue as red.global.add.f64 of -acc (no C load)
     int ntiles;          // tiles_m * tiles_n; CTA b owns tiles b, b + gridDim.x, ...
     int tiles_per_cta;
 };
@@ -107,6 +108,11 @@ __device__ __forceinline__ double2 lds128(uint32_t addr)
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
     return v;
+}
+
+__device__ __forceinline__ void red_add(double *p, double v)
+{
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0)
@@ -298,7 +304,14 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
                 // row 2g: lo.c0 hi.c0 lo.c1 hi.c1 ; row 2g+1: lo.c2 hi.c2 lo.c3 hi.c3
                 const double v0 = acc[i][j][0][2 * h], v1 = acc[i][j][1][2 * h];
                 const double v2 = acc[i][j][0][2 * h + 1], v3 = acc[i][j][1][2 * h + 1];
-                if (vec_ok && col + 3 < p.n) {
+                if (p.red_epi && p.mode == GEMM_UPDATE) {
+                    // C + (-acc) performed at L2: one rounding, as C - acc; the
+                    // warp does not wait for C (each element is touched once)
+                    if (col + 0 < p.n) red_add(crow + col + 0, -v0);
+                    if (col + 1 < p.n) red_add(crow + col + 1, -v1);
+                    if (col + 2 < p.n) red_add(crow + col + 2, -v2);
+                    if (col + 3 < p.n) red_add(crow + col + 3, -v3);
+                } else if (vec_ok && col + 3 < p.n) {
                     double2 *q = reinterpret_cast<double2 *>(crow + col);
                     if (p.mode == GEMM_UPDATE) {
                         double2 x0 = q[0], x1 = q[1];
@@ -378,9 +391,12 @@ using CfgB = Cfg<128, 128, 64, 32, 6, 1>;
 using CfgC = Cfg<64, 64, 32, 32, 4, 3>;
 // 64x64 tile, 2 CTAs/SM, 6 stages (tuning variant).
 using CfgD = Cfg<64, 64, 32, 32, 6, 2>;
+// 64x64 tile, 4 CTAs/SM, 3 stages (more warps to cover epilogues).
+using CfgE = Cfg<64, 64, 32, 32, 3, 4>;
 
 int g_default_cfg = 2;
 int g_tiles_per_cta = 1;
+int g_red_epi = 0;
 
 template <class C, int SLOT>
 cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
@@ -420,6 +436,7 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
 
 void dgemm_set_default_cfg(int cfg) { g_default_cfg = cfg; }
 void dgemm_set_tiles_per_cta(int t) { g_tiles_per_cta = t > 0 ? t : 1; }
+void dgemm_set_red_epilogue(int on) { g_red_epi = on; }
 int dgemm_get_default_cfg() { return g_default_cfg; }
 
 cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n, int64_t k,
@@ -453,11 +470,13 @@ cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n,
     p.C2 = C2; p.ldc2 = ldc2;
     p.prefetch_c = 1;
     p.zero = 0;
+    p.red_epi = g_red_epi;
     if (cfg < 0) cfg = g_default_cfg;
     switch (cfg) {
     case 1: return launch_cfg<CfgB>(st, ma, mb, p, slot);
     case 2: return launch_cfg<CfgC>(st, ma, mb, p, slot);
     case 3: return launch_cfg<CfgD>(st, ma, mb, p, slot);
+    case 4: return launch_cfg<CfgE>(st, ma, mb, p, slot);
     default: return launch_cfg<CfgA>(st, ma, mb, p, slot);
     }
 }

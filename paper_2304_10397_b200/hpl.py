@@ -270,3 +270,11 @@ def hplk_dmma_peak(iters: int = 20000, blocks_per_sm: int = 2, warps: int = 8) -
     o = np.zeros(2, dtype=np.float64)
     _k(lib.hplk_dmma_peak(iters, blocks_per_sm, warps, ptr(o)), "hplk_dmma_peak")
     return o[1] / (o[0] * 1e-3) / 1e12
+
+
+def hplk_panel_bench(m: int, nb: int = 512, nbmin: int = 16, leaf_ctas: int = 0,
+                     reps: int = 3) -> np.ndarray:
+    """Per-rep device time (ms) of the panel FACT of an m x nb panel."""
+    ms = np.zeros(reps, dtype=np.float64)
+    _k(lib.hplk_panel_bench(m, nb, nbmin, leaf_ctas, reps, ptr(ms)), "hplk_panel_bench")
+    return ms

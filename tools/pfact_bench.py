@@ -1,0 +1,17 @@
+"""Device analog of PAPER.md Fig. pfact-mptest: panel FACT GFLOP/s of M x 512
+panels (recursive right-looking, NDIV=2, base 16) vs M, for several leaf grid
+widths (the device counterpart of the paper's CPU thread counts).  Flop count
+M*NB^2 - NB^3/3.  Prints one JSON line per point."""
+import json
+import sys
+
+import paper_2304_10397_b200 as H
+
+NB = 512
+Ms = [int(v) for v in sys.argv[1:]] or [1024, 2048, 4096, 8192, 16384, 32768, 65536, 131072]
+for M in Ms:
+    for ctas in (1, 2, 4, 8, 16, 32, 64, 148):
+        ms = H.hplk_panel_bench(M, NB, 16, ctas, reps=3)
+        fl = M * NB ** 2 - NB ** 3 / 3
+        print(json.dumps(dict(M=M, NB=NB, leaf_ctas=ctas, ms=round(float(min(ms)), 3),
+                              gflops=round(fl / (min(ms) * 1e-3) / 1e9, 1))), flush=True)
