@@ -1,0 +1,205 @@
+"""Timeline analysis and cost model for the HPL schedule (host-side, no GPU).
+
+SURVEY.md §8(f) NEXT 2 and NEXT 4; PAPER.md l.70–84 (Fig. iteration, two
+regimes), l.64 (hiding persistence), l.66 (split fraction)
+(metrics-timeline: IterationTrace, overlap_fraction, predict_crossover,
+tune_split).
+
+Traces come from ``hpl_get_timeline`` (CUDA events inside libhpl): per
+iteration j the ms spent in [FACT(j+1), look-ahead update, rest update, rest
+RS/LASWP, rest DTRSM, rest DGEMM].  With depth-1 look-ahead the iteration's
+critical path is max(rest, la + fact): the iteration is *hidden* when the
+look-ahead chain (update of the next panel, FACT, LBCAST) fits under the
+trailing update, *exposed* otherwise.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, List, Sequence
+
+import numpy as np
+
+QUANTUM = 0.05  # hidden <=> t_iter - t_engine <= 5 % of t_iter
+
+
+@dataclass
+class IterationTrace:
+    j: int
+    fact: float
+    la: float
+    rest: float
+    rs: float
+    trsm: float
+    dgemm: float
+
+    @property
+    def t_iter(self) -> float:
+        """Critical path of the iteration under depth-1 look-ahead."""
+        return max(self.rest, self.la + self.fact)
+
+    @property
+    def t_engine(self) -> float:
+        """Time the trailing-update engine is busy (the Fig. iteration 'GPU active')."""
+        return self.rest
+
+
+def traces_from_timeline(tl) -> List[IterationTrace]:
+    tl = np.asarray(tl, dtype=np.float64).reshape(-1, 6)
+    return [IterationTrace(j, *map(float, row)) for j, row in enumerate(tl)]
+
+
+def regime(t: IterationTrace, quantum: float = QUANTUM) -> str:
+    return "hidden" if t.t_iter - t.t_engine <= quantum * t.t_iter else "exposed"
+
+
+def overlap_fraction(traces: Sequence[IterationTrace], quantum: float = QUANTUM) -> float:
+    """Share of the run spent in hidden iterations (PAPER.md l.64 quotes ~75 %
+    for rocHPL on one Frontier node): sum t_iter(hidden) / sum t_iter."""
+    tot = sum(t.t_iter for t in traces)
+    if tot <= 0:
+        return 0.0
+    return sum(t.t_iter for t in traces if regime(t, quantum) == "hidden") / tot
+
+
+def crossover(traces: Sequence[IterationTrace], quantum: float = QUANTUM) -> int:
+    """First iteration from which every later iteration is exposed (the
+    Fig. iteration regime change); len(traces) if the run never crosses.  The
+    last iteration has no next panel (no FACT, no look-ahead) and is neutral."""
+    k = max(len(traces) - 1, 0)
+    end = k
+    while k > 0 and regime(traces[k - 1], quantum) == "exposed":
+        k -= 1
+    return k if k < end else len(traces)
+
+
+# ----------------------------------------------------------------------------- model
+@dataclass
+class CostModel:
+    """Per-phase costs (ms) as linear functions of the iteration's local sizes.
+
+    rest  = c_gemm * 2 m n jb              (trailing DTRSM + DGEMM, flop-bound)
+    la    = c_gemm * 2 m jb jb             (look-ahead update of jb columns)
+    fact  = c_fact0 + c_fact1 * m          (latency floor + per-row work)
+    rs    = c_rs * n jb                    (row-swap bytes)
+    bcast = c_bcast * m jb                 (LBCAST bytes, 0 on one process column)
+    """
+    c_gemm: float
+    c_fact0: float
+    c_fact1: float
+    c_rs: float = 0.0
+    c_bcast: float = 0.0
+
+    def phases(self, m: float, n: float, jb: float) -> dict:
+        return dict(rest=self.c_gemm * 2 * m * n * jb + self.c_rs * n * jb,
+                    la=self.c_gemm * 2 * m * jb * jb,
+                    fact=self.c_fact0 + self.c_fact1 * m + self.c_bcast * m * jb,
+                    rs=self.c_rs * n * jb)
+
+
+def local_sizes(N: int, NB: int, P: int = 1, Q: int = 1):
+    """(m_j, n_j, jb_j) per iteration: local rows at/below block row j and local
+    trailing columns (incl. b) of one process, the average over the grid."""
+    out = []
+    for j in range(-(-N // NB)):
+        j0 = j * NB
+        jb = min(NB, N - j0)
+        out.append(((N - j0) / P, (N + 1 - j0 - jb) / Q, jb))
+    return out
+
+
+def _features(N: int, NB: int, P: int, Q: int):
+    """Per iteration j: (m, n, jb) of the trailing update and m' = rows of the
+    NEXT panel (FACT(j+1) and the look-ahead update act on it; 0 at the end)."""
+    sz = local_sizes(N, NB, P, Q)
+    nxt = [sz[j + 1][0] if j + 1 < len(sz) else 0.0 for j in range(len(sz))]
+    njb = [sz[j + 1][2] if j + 1 < len(sz) else 0 for j in range(len(sz))]
+    return sz, nxt, njb
+
+
+def predict(model: CostModel, N: int, NB: int, P: int = 1, Q: int = 1) -> List[IterationTrace]:
+    tr = []
+    sz, nxt, njb = _features(N, NB, P, Q)
+    for j, (m, n, jb) in enumerate(sz):
+        rest = model.c_gemm * 2 * m * n * jb + model.c_rs * n * jb
+        la = model.c_gemm * 2 * nxt[j] * jb * njb[j]
+        fact = (model.c_fact0 + model.c_fact1 * nxt[j] + model.c_bcast * nxt[j] * njb[j]
+                if njb[j] else 0.0)
+        rs = model.c_rs * n * jb
+        tr.append(IterationTrace(j, fact, la, rest, rs, 0.0, rest - rs))
+    return tr
+
+
+def predict_crossover(model: CostModel, N: int, NB: int, P: int = 1, Q: int = 1,
+                      quantum: float = QUANTUM) -> int:
+    return crossover(predict(model, N, NB, P, Q), quantum)
+
+
+def fit(traces: Sequence[IterationTrace], N: int, NB: int, P: int = 1, Q: int = 1) -> CostModel:
+    """Least-squares fit of the model's coefficients to measured traces."""
+    sz, nxt, njb = _features(N, NB, P, Q)
+    k = len(traces)
+    sz, nxt, njb = sz[:k], np.array(nxt[:k]), np.array(njb[:k])
+    m = np.array([s[0] for s in sz]); n = np.array([s[1] for s in sz]); jb = np.array([s[2] for s in sz])
+    rest = np.array([t.rest for t in traces]); fact = np.array([t.fact for t in traces])
+    rs = np.array([t.rs for t in traces])
+    gflop = 2 * m * n * jb
+    ok = gflop > 0
+    c_gemm = float(np.dot(gflop[ok], rest[ok] - rs[ok]) / np.dot(gflop[ok], gflop[ok]))
+    has = njb > 0
+    X = np.stack([np.ones_like(nxt[has]), nxt[has]], 1)
+    c_fact0, c_fact1 = (float(v) for v in np.linalg.lstsq(X, fact[has], rcond=None)[0])
+    byt = n * jb
+    c_rs = float(np.dot(byt, rs) / max(np.dot(byt, byt), 1e-300))
+    return CostModel(c_gemm=c_gemm, c_fact0=max(c_fact0, 0.0), c_fact1=max(c_fact1, 0.0),
+                     c_rs=max(c_rs, 0.0))
+
+
+# ----------------------------------------------------------------------------- split update
+def split_iteration_hidden(model: CostModel, m: float, n1: float, n2: float, jb: float) -> bool:
+    """Split update: UPDATE2 (right, n2 columns) must hide
+    the look-ahead chain and RS1 (the left section's row swaps)."""
+    upd2 = model.c_gemm * 2 * m * n2 * jb
+    hidden = (model.c_gemm * 2 * m * jb * jb + model.c_fact0 + model.c_fact1 * m
+              + model.c_bcast * m * jb + model.c_rs * n1 * jb)
+    return upd2 >= hidden
+
+
+def tune_split(model: CostModel, N: int, NB: int, P: int = 1, Q: int = 1) -> float:
+    """Smallest right-section fraction n2/n (n2 a multiple of NB) whose UPDATE2
+    hides the look-ahead chain and RS1 at iteration 0 (SPEC.md tune_split);
+    1.0 if no fraction suffices."""
+    m, n, jb = local_sizes(N, NB, P, Q)[0]
+    for k in range(1, int(n // NB) + 1):
+        n2 = k * NB
+        if split_iteration_hidden(model, m, max(n - n2, 0.0), n2, jb):
+            return n2 / n
+    return 1.0
+
+
+def hiding_persists(model: CostModel, N: int, NB: int, frac: float, P: int = 1,
+                    Q: int = 1) -> bool:
+    """with n2 fixed, UPDATE2 and the hidden phases both scale
+    linearly in m (RS1 in n1, which shrinks), so if UPDATE2 hides them at the
+    start it keeps hiding them while n1 > 0.  Checks that on the model."""
+    sizes = local_sizes(N, NB, P, Q)
+    n_local = sizes[0][1]
+    n2 = max(NB, round(frac * n_local / NB) * NB)
+    first = True
+    for (m, n, jb) in sizes:
+        n1 = n - n2
+        if n1 <= 0:
+            break
+        ok = split_iteration_hidden(model, m, n1, n2, jb)
+        if first and not ok:
+            return True  # the premise does not hold: nothing to check
+        first = False
+        if not ok:
+            return False
+    return True
+
+
+def summary(traces: Sequence[IterationTrace]) -> dict:
+    return dict(iterations=len(traces), crossover=crossover(traces),
+                overlap_fraction=overlap_fraction(traces),
+                t_iter_ms=sum(t.t_iter for t in traces),
+                exposed_ms=sum(max(0.0, t.la + t.fact - t.rest) for t in traces))

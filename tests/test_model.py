@@ -1,0 +1,92 @@
+"""CPU tests of the timeline analysis / cost model (paper_2304_10397_b200/model.py),
+pinned to closed forms and the properties SPEC.md l.467–470 states."""
+import importlib.util
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_spec = importlib.util.spec_from_file_location(
+    "hpl_model", os.path.join(ROOT, "paper_2304_10397_b200", "model.py"))
+M = importlib.util.module_from_spec(_spec)
+sys.modules["hpl_model"] = M
+_spec.loader.exec_module(M)
+
+
+def _tr(rows):
+    return M.traces_from_timeline(np.array(rows, dtype=float))
+
+
+def test_overlap_fraction_extremes():
+    # all hidden -> 1.0, none hidden -> 0.0
+    hidden = _tr([[1, 1, 10, 0, 0, 10]] * 5)
+    exposed = _tr([[10, 1, 2, 0, 0, 2]] * 5)
+    assert M.overlap_fraction(hidden) == 1.0
+    assert M.overlap_fraction(exposed) == 0.0
+    assert M.crossover(hidden) == 5 and M.crossover(exposed) == 0
+
+
+def test_two_regime_crossover_and_fraction():
+    # rest shrinks quadratically, fact linearly: one hidden->exposed transition
+    rows = []
+    for j in range(100):
+        s = 1 - j / 100
+        rows.append([5 * s + 1, 0.1, 100 * s * s, 0, 0, 100 * s * s])
+    tr = _tr(rows)
+    k = M.crossover(tr)
+    regimes = [M.regime(t) for t in tr]
+    assert all(r == "hidden" for r in regimes[:k]) and all(r == "exposed" for r in regimes[k:])
+    # exact crossover of 100 s^2 vs 5 s + 1.1 (quantum 5 %): first s where exposed
+    s = 1 - np.arange(100) / 100
+    exposed = (np.maximum(100 * s * s, 5 * s + 1.1) - 100 * s * s) > 0.05 * np.maximum(100 * s * s, 5 * s + 1.1)
+    assert k == int(np.argmax(exposed))
+    assert 0.0 < M.overlap_fraction(tr) < 1.0
+
+
+def test_zero_fact_cost_never_crosses():
+    # zero communication / FACT cost -> crossover at the end
+    m = M.CostModel(c_gemm=1e-9, c_fact0=0.0, c_fact1=0.0)
+    assert M.predict_crossover(m, 8192, 256) >= len(M.local_sizes(8192, 256)) - 1
+
+
+def test_dominant_fact_crosses_at_zero():
+    m = M.CostModel(c_gemm=1e-12, c_fact0=1e6, c_fact1=0.0)
+    assert M.predict_crossover(m, 8192, 256) == 0
+
+
+def test_crossover_monotone_in_fact_cost():
+    # raising a hidden-phase coefficient never delays the crossover
+    ks = [M.predict_crossover(M.CostModel(3e-11, f, 1e-5), 131072, 512) for f in (0.5, 2, 8, 32)]
+    assert all(a >= b for a, b in zip(ks, ks[1:]))
+
+
+def test_fit_recovers_coefficients():
+    true = M.CostModel(c_gemm=2.8e-11, c_fact0=4.5, c_fact1=2.0e-4, c_rs=3e-6)
+    tr = M.predict(true, 65536, 512, 2, 2)
+    got = M.fit(tr, 65536, 512, 2, 2)
+    assert got.c_gemm == pytest.approx(true.c_gemm, rel=1e-9)
+    assert got.c_fact0 == pytest.approx(true.c_fact0, rel=1e-6)
+    assert got.c_fact1 == pytest.approx(true.c_fact1, rel=1e-6)
+    assert got.c_rs == pytest.approx(true.c_rs, rel=1e-6)
+
+
+def test_tune_split_properties():
+    # zero hidden-phase cost -> the minimal fraction NB / n (SPEC tune_split example)
+    m0 = M.CostModel(c_gemm=1e-11, c_fact0=0.0, c_fact1=0.0)
+    n = M.local_sizes(65536, 512, 2, 2)[0][1]
+    assert M.tune_split(m0, 65536, 512, 2, 2) == pytest.approx(512 / n)
+    # a heavier FACT needs a larger right section
+    a = M.tune_split(M.CostModel(1e-11, 50.0, 1e-4, c_rs=1e-6), 65536, 512, 2, 2)
+    b = M.tune_split(M.CostModel(1e-11, 200.0, 1e-4, c_rs=1e-6), 65536, 512, 2, 2)
+    assert a <= b <= 1.0
+
+
+def test_hiding_persistence():
+    # hidden at the start => hidden while n1 > 0 (linear-in-m costs)
+    for c in [M.CostModel(1e-11, 0.0, 1e-4, c_rs=1e-6, c_bcast=1e-7),
+              M.CostModel(3e-11, 0.0, 5e-4, c_rs=5e-6)]:
+        f = M.tune_split(c, 131072, 512, 2, 2)
+        if f < 1.0:
+            assert M.hiding_persists(c, 131072, 512, f, 2, 2)
