@@ -31,16 +31,18 @@ class IterationTrace:
     rs: float
     trsm: float
     dgemm: float
+    wall: float = 0.0     # replayed iteration time (0: derive from the phases)
+    engine: float = 0.0   # replayed engine busy time (0: the rest phase)
 
     @property
     def t_iter(self) -> float:
         """Critical path of the iteration under depth-1 look-ahead."""
-        return max(self.rest, self.la + self.fact)
+        return self.wall if self.wall > 0 else max(self.rest, self.la + self.fact)
 
     @property
     def t_engine(self) -> float:
         """Time the trailing-update engine is busy (the Fig. iteration 'GPU active')."""
-        return self.rest
+        return self.engine if self.wall > 0 else self.rest
 
 
 def traces_from_timeline(tl) -> List[IterationTrace]:
@@ -203,3 +205,115 @@ def summary(traces: Sequence[IterationTrace]) -> dict:
                 overlap_fraction=overlap_fraction(traces),
                 t_iter_ms=sum(t.t_iter for t in traces),
                 exposed_ms=sum(max(0.0, t.la + t.fact - t.rest) for t in traces))
+
+
+# ----------------------------------------------------------------------------- replay
+@dataclass
+class Replay:
+    makespan: float
+    traces: List[IterationTrace]
+
+
+def _overlap(a0, a1, b0, b1):
+    return max(0.0, min(a1, b1) - max(a0, b0))
+
+
+def replay(model: CostModel, N: int, NB: int, P: int = 1, Q: int = 1, lookahead: bool = True,
+           split: float = 0.0, alpha: float = 0.0) -> Replay:
+    """Discrete-event replay of libhpl's stream schedule with model costs
+    (SPEC.md MODEL mode).  Streams as in hpl_driver.cu:
+    S_la (look-ahead update of panel j+1's columns, then FACT(j+1) after the
+    trailing RS of iteration j), S_tr (trailing RS then DGEMM), and with
+    ``split`` > 0 a third stream S_rs that runs RS_R(j), RS_L(j) while S_tr runs
+    UPDATE_R(j), UPDATE_L(j) (the right section is a fixed
+    NB-multiple share of the local columns, the schedule falls back once the
+    left section is empty).  ``alpha`` stretches the trailing DGEMM by
+    alpha × its overlap with a concurrent FACT (the SM-sharing slowdown).
+    Per-iteration traces: t_iter = time between successive "trailing update
+    of iteration j done and panel j+1 factored" marks, t_engine = DGEMM busy
+    time, so the regime test of ``regime`` applies unchanged."""
+    sz = local_sizes(N, NB, P, Q)
+    J = len(sz)
+    nxt = [sz[j + 1][0] if j + 1 < J else 0.0 for j in range(J)]
+    njb = [sz[j + 1][2] if j + 1 < J else 0 for j in range(J)]
+    fact_cost = [model.c_fact0 + model.c_fact1 * sz[0][0] + model.c_bcast * sz[0][0] * sz[0][2]]
+    fact_cost += [(model.c_fact0 + model.c_fact1 * nxt[j] + model.c_bcast * nxt[j] * njb[j])
+                  if njb[j] else 0.0 for j in range(J)]
+    n2 = 0.0
+    if split > 0:
+        n2 = max(NB, round(split * sz[0][1] / NB) * NB) / 1.0
+    fact_end = fact_cost[0]
+    la_free = fact_end
+    tr_free = 0.0
+    rs_free = 0.0
+    updR_end = updL_end = 0.0
+    prev_mark = fact_end  # FACT(0) precedes iteration 0
+    prev_rest_end = 0.0
+    traces = []
+    for j, (m, n, jb) in enumerate(sz):
+        n_rest = max(n - njb[j], 0.0) if lookahead else n
+        la = model.c_gemm * 2 * nxt[j] * jb * njb[j] if lookahead else 0.0
+        fcost = fact_cost[j + 1]
+        if not lookahead:
+            rs_s = max(tr_free, fact_end)
+            rs_e = rs_s + model.c_rs * n * jb
+            up_e = rs_e + model.c_gemm * 2 * m * n * jb
+            f_e = up_e + fcost
+            tr_free = f_e
+            mark = f_e
+            traces.append(IterationTrace(j, fcost, 0.0, up_e - rs_s, rs_e - rs_s, 0.0, up_e - rs_e,
+                                         wall=mark - prev_mark, engine=up_e - rs_s))
+            fact_end = f_e
+            prev_mark = mark
+            continue
+        # S_la: look-ahead update of panel j+1's columns (needs rest(j-1), FACT(j))
+        la_s = max(la_free, fact_end, prev_rest_end)
+        la_e = la_s + la
+        n1 = n_rest - n2
+        if split > 0 and n1 > 0:
+            # S_rs: RS_R(j) then RS_L(j); S_tr: UPDATE_R(j) then UPDATE_L(j)
+            rsR_s = max(rs_free, fact_end, updR_end)
+            rsR_e = rsR_s + model.c_rs * n2 * jb
+            rsL_s = max(rsR_e, updL_end)
+            rsL_e = rsL_s + model.c_rs * n1 * jb
+            rs_free = rsL_e
+            f_s = max(la_e, rsR_e)
+            f_e = f_s + fcost
+            uR_s = max(tr_free, rsR_e)
+            uR_d = model.c_gemm * 2 * m * n2 * jb
+            uR_e = uR_s + uR_d
+            uR_e += alpha * _overlap(uR_s, uR_e, f_s, f_e)
+            uL_s = max(uR_e, rsL_e)
+            uL_d = model.c_gemm * 2 * m * n1 * jb
+            uL_e = uL_s + uL_d
+            uL_e += alpha * _overlap(uL_s, uL_e, f_s, f_e)
+            updR_end, updL_end = uR_e, uL_e
+            rest_s, rs_e, rest_e = uR_s, rsL_e, uL_e
+            dg = (uR_e - uR_s) + (uL_e - uL_s)
+            rs_d = (rsR_e - rsR_s) + (rsL_e - rsL_s)
+        else:
+            rs_s = max(tr_free, fact_end, rs_free)
+            rs_e = rs_s + model.c_rs * n_rest * jb
+            f_s = max(la_e, rs_e)
+            f_e = f_s + fcost
+            up_d = model.c_gemm * 2 * m * n_rest * jb
+            up_e = rs_e + up_d
+            up_e += alpha * _overlap(rs_e, up_e, f_s, f_e)
+            rest_s, rest_e = rs_s, up_e
+            dg = up_e - rs_e
+            rs_d = rs_e - rs_s
+            updR_end = updL_end = rs_free = up_e
+        tr_free = rest_e
+        la_free = f_e
+        mark = max(rest_e, f_e)
+        # trace: la+fact on S_la vs the engine's busy time in this iteration
+        traces.append(IterationTrace(j, f_e - f_s, la_e - la_s, dg + rs_d, rs_d, 0.0, dg,
+                                     wall=max(mark - prev_mark, 1e-300), engine=dg + rs_d))
+        prev_rest_end = rest_e
+        fact_end = f_e
+        prev_mark = mark
+    return Replay(makespan=prev_mark, traces=traces)
+
+
+def replay_regimes(rep: Replay, quantum: float = QUANTUM) -> List[str]:
+    return [regime(t, quantum) for t in rep.traces]

@@ -90,3 +90,71 @@ def test_hiding_persistence():
         f = M.tune_split(c, 131072, 512, 2, 2)
         if f < 1.0:
             assert M.hiding_persists(c, 131072, 512, f, 2, 2)
+
+
+# ---- discrete-event replay (SPEC.md MODEL mode)
+def _rand_models(k, seed=0):
+    rng = np.random.default_rng(seed)
+    return [M.CostModel(c_gemm=rng.uniform(1e-11, 4e-11), c_fact0=rng.uniform(0, 20),
+                        c_fact1=rng.uniform(0, 5e-4), c_rs=rng.uniform(0, 2e-8))
+            for _ in range(k)]
+
+
+def test_replay_lookahead_matches_recurrence():
+    # independent statement of the depth-1 look-ahead critical path (rs = 0):
+    # R_j = max(R_{j-1}, F_j) + u_j ;  F_{j+1} = max(F_j, R_{j-1}) + la_j + f_{j+1}
+    c = M.CostModel(c_gemm=3e-11, c_fact0=7.0, c_fact1=2e-4)
+    N, NB = 32768, 512
+    s = M.local_sizes(N, NB)
+    J = len(s)
+    f = [c.c_fact0 + c.c_fact1 * s[0][0]] + [c.c_fact0 + c.c_fact1 * s[j + 1][0] if j + 1 < J else 0.0
+                                            for j in range(J)]
+    R_prev, F = 0.0, f[0]
+    for j, (m, n, jb) in enumerate(s):
+        nj = s[j + 1][2] if j + 1 < J else 0
+        mj = s[j + 1][0] if j + 1 < J else 0.0
+        u = c.c_gemm * 2 * m * max(n - nj, 0) * jb
+        la = c.c_gemm * 2 * mj * jb * nj
+        R = max(R_prev, F) + u
+        F = max(F, R_prev) + la + f[j + 1]
+        R_prev = R
+    assert M.replay(c, N, NB).makespan == pytest.approx(max(R_prev, F), rel=1e-12)
+
+
+def test_replay_no_lookahead_closed_form():
+    c = M.CostModel(c_gemm=3e-11, c_fact0=7.0, c_fact1=2e-4, c_rs=1e-8)
+    N, NB = 32768, 512
+    s = M.local_sizes(N, NB)
+    tot = c.c_fact0 + c.c_fact1 * N
+    for j, (m, n, jb) in enumerate(s):
+        tot += c.c_rs * n * jb + c.c_gemm * 2 * m * n * jb
+        if j + 1 < len(s):
+            tot += c.c_fact0 + c.c_fact1 * s[j + 1][0]
+    assert M.replay(c, N, NB, lookahead=False).makespan == pytest.approx(tot, rel=1e-12)
+
+
+def test_replay_lookahead_never_slower_and_crossover_agrees():
+    # SPEC.md: predicted crossover within +-2 iterations of the simulated flip
+    for c in _rand_models(5):
+        la = M.replay(c, 65536, 512)
+        assert la.makespan <= M.replay(c, 65536, 512, lookahead=False).makespan * (1 + 1e-12)
+        assert abs(M.crossover(la.traces) - M.predict_crossover(c, 65536, 512)) <= 2
+        reg = M.replay_regimes(la)[:-1]
+        flips = sum(1 for a, b in zip(reg, reg[1:]) if a != b)
+        assert flips <= 1 and (not reg or reg[0] == "hidden" or "hidden" not in reg)
+
+
+def test_replay_split_degenerates_and_persists():
+    c = M.CostModel(c_gemm=1e-11, c_fact0=0.0, c_fact1=1e-4, c_rs=5e-6)
+    N, NB = 65536, 512
+    # right section covering all columns -> the unsplit schedule
+    assert M.replay(c, N, NB, split=1.0).makespan == pytest.approx(M.replay(c, N, NB).makespan,
+                                                                    rel=1e-12)
+    # hidden at iteration 0 -> hidden while the left section is non-empty
+    f = M.tune_split(c, N, NB)
+    assert f < 1.0
+    rep = M.replay(c, N, NB, split=f)
+    n2 = max(NB, round(f * M.local_sizes(N, NB)[0][1] / NB) * NB)
+    for t, (m, n, jb) in zip(rep.traces, M.local_sizes(N, NB)):
+        if n - jb - n2 > 0:
+            assert M.regime(t) == "hidden", t.j

@@ -64,6 +64,10 @@ def main():
                     dgemm_tflops=round(tm["dgemm_flop"] / max(tm["dgemm_ms"], 1e-9) / 1e9, 2),
                     fact_iter0=round(float(fact[0]), 2), rest_iter0=round(float(rest[0]), 2))
         print(json.dumps(summ), flush=True)
+        for a in sys.argv[1:]:
+            if a.startswith("--timeline-out="):
+                np.savetxt(f"{a.split('=', 1)[1]}_r{rank}.csv", tl, delimiter=",", fmt="%.4f",
+                           header="fact,la_update,rest_update,rest_rs,rest_trsm,rest_dgemm")
     ipiv = H.hpl_get_ipiv(ctx)
     r = H.hpl_residual(ctx)
     H.hpl_free(ctx)

@@ -24,5 +24,9 @@ tr = M.traces_from_timeline(np.loadtxt(f, delimiter=",", skiprows=1))
 c = M.fit(tr, N, NB, P, Q)
 pred = M.predict(c, N, NB, P, Q)
 out = dict(measured=M.summary(tr), regimes="".join("H" if M.regime(t) == "hidden" else "x" for t in tr),
-           model=c.__dict__, predicted=M.summary(pred), tune_split=M.tune_split(c, N, NB, P, Q))
+           model=c.__dict__, predicted=M.summary(pred), tune_split=M.tune_split(c, N, NB, P, Q),
+           replay_ms={"lookahead": M.replay(c, N, NB, P, Q).makespan,
+                      "no_lookahead": M.replay(c, N, NB, P, Q, lookahead=False).makespan,
+                      **{f"split_{f}": M.replay(c, N, NB, P, Q, split=f).makespan
+                         for f in (0.1, 0.25, 0.5)}})
 print(json.dumps(out, indent=1))
