@@ -111,6 +111,13 @@ hpl_status hpl_get_local(const hpl_ctx *ctx, double *host, int64_t ld);
  * [fact, la_update, rest_update, laswp, trsm, dgemm_rest]; returns the number
  * of iterations written (<= cap). */
 int64_t hpl_get_timeline(const hpl_ctx *ctx, double *t, int64_t cap);
+/* Breakdown of the timeline's fact phase, 3 doubles per iteration j (ms):
+ * [wait for the trailing RS + DTRSM of iteration j before FACT(j+1),
+ *  FACT(j+1) proper on the owner process column (0 elsewhere: pack, factor,
+ *  write back, incl. the P>1 pivot exchange), LBCAST(j+1) + pivot plan +
+ *  L11^{-1}].  Zeros for the last iteration.  Needs hpl_set_timing(ctx, 1)
+ * before hpl_factor; returns the number of iterations written (<= cap). */
+int64_t hpl_get_fact_detail(const hpl_ctx *ctx, double *t, int64_t cap);
 /* Enable per-phase CUDA events (adds a little host work per iteration). */
 hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
 /* Tuning knobs: lookahead on/off (default on). */

@@ -50,6 +50,7 @@ _sig("hpl_singular_column", i64, [ctx_p])
 _sig("hpl_get_ipiv", ctypes.c_int, [ctx_p, vp])
 _sig("hpl_get_local", ctypes.c_int, [ctx_p, vp, i64])
 _sig("hpl_get_timeline", i64, [ctx_p, vp, i64])
+_sig("hpl_get_fact_detail", i64, [ctx_p, vp, i64])
 _sig("hpl_set_timing", ctypes.c_int, [ctx_p, i32])
 _sig("hpl_set_option", ctypes.c_int, [ctx_p, ctypes.c_char_p, i64])
 _sig("hpl_launch_count", i64, [ctx_p])
@@ -73,7 +74,7 @@ EXPORTED = [
     "hpl_init", "hpl_init_dist", "hpl_get_unique_id", "hpl_factor", "hpl_solve",
     "hpl_residual", "hpl_regenerate", "hpl_load_local", "hpl_local_shape", "hpl_free",
     "hpl_last_error", "hpl_singular_column", "hpl_get_ipiv", "hpl_get_local",
-    "hpl_get_timeline", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
+    "hpl_get_timeline", "hpl_get_fact_detail", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
     "hpl_last_timing", "hpl_plan_iteration", "hpl_pin_host",
     "hplk_dgemm_update", "hplk_trsm", "hplk_panel_fact", "hplk_laswp", "hplk_back_solve",
     "hplk_generate", "hplk_maxloc", "hplk_dgemm_bench", "hplk_dmma_peak", "hplk_panel_bench",

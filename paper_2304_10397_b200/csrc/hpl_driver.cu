@@ -84,6 +84,7 @@ struct hpl_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> tev;   // 7 events per iteration when timing
     std::vector<double> timeline;   // 6 values per iteration (ms)
+    std::vector<double> fact_detail;  // 3 values per iteration (ms)
     cudaEvent_t ev_t[3] = {nullptr, nullptr, nullptr};  // factor start/end, solve end
     double factor_ms = 0, solve_ms = 0;
     double dgemm_ms = 0, dgemm_flop = 0;   // trailing (rest) DGEMM launches, timing on
@@ -212,8 +213,10 @@ hpl_status lbcast_and_plan(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 }
 
 // FACT(j) (owner column) + LBCAST(j) + plan (everyone).
-hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
+hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b, cudaEvent_t ev_pre = nullptr,
+                      cudaEvent_t ev_mid = nullptr)
 {
+    if (ev_pre) CK(c, cudaEventRecord(ev_pre, st));
     if (c->leaf_auto) {
         // The leaf is latency-bound.  While a long trailing DGEMM runs beside it
         // (FACT hidden), a few CTAs leave the SMs to the DGEMM; once the
@@ -227,6 +230,7 @@ hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
         hpl_status s = fact_local(c, st, j, b);
         if (s != HPL_OK) return s;
     }
+    if (ev_mid) CK(c, cudaEventRecord(ev_mid, st));
     return lbcast_and_plan(c, st, j, b);
 }
 
@@ -335,7 +339,7 @@ hpl_status update_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0
 
 hpl_status ensure_timing_events(hpl_ctx *c, int64_t nblk)
 {
-    const size_t need = (size_t)(7 * nblk);
+    const size_t need = (size_t)(10 * nblk);
     if (c->tev.size() == need) return HPL_OK;
     for (auto e : c->tev) cudaEventDestroy(e);
     c->tev.assign(need, nullptr);
@@ -384,7 +388,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     if (!M((void **)&c->U2, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
     if (!M((void **)&c->scratch, sizeof(double) * round_up(NBs, 16) * NBs)) return HPL_ERR_OOM;
     if (!M((void **)&c->x, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
-    if (!M((void **)&c->tbuf, sizeof(double) * NBs)) return HPL_ERR_OOM;
+    if (!M((void **)&c->tbuf, sizeof(double) * 16 * NBs)) return HPL_ERR_OOM;
     if (!M((void **)&c->out4, sizeof(double) * 4)) return HPL_ERR_OOM;
     if (!M((void **)&c->rvec, sizeof(double) * (size_t)std::max<int64_t>(c->mloc, 1))) return HPL_ERR_OOM;
     if (!M((void **)&c->avec, sizeof(double) * (size_t)std::max<int64_t>(c->mloc, 1))) return HPL_ERR_OOM;
@@ -603,7 +607,7 @@ hpl_status hpl_factor(hpl_ctx *c)
         // panel j+1 lives in the next jb1 local columns of its owner column
         const bool own_next = has_next && c->mycol == (int)((j + 1) % c->Q);
         const int64_t lrest = lct + (own_next ? jb1 : 0);
-        cudaEvent_t *E = c->timing ? &c->tev[7 * j] : nullptr;
+        cudaEvent_t *E = c->timing ? &c->tev[10 * j] : nullptr;
         if (c->lookahead && split) {
             // Split update: right section [cs, cend) (fixed width n2, holds b) and
             // left section [lrest, cs).  S_rs runs RS_R(j) then RS_L(j); S_tr runs
@@ -687,7 +691,7 @@ hpl_status hpl_factor(hpl_ctx *c)
             // critical path of S_tr) finish first; FACT then overlaps the DGEMM.
             if (has_next) CK(c, cudaStreamWaitEvent(c->s_la, c->ev_trsm, 0));
             if (has_next) {
-                s = fact_panel(c, c->s_la, j + 1, bn);
+                s = fact_panel(c, c->s_la, j + 1, bn, E ? E[7] : nullptr, E ? E[8] : nullptr);
                 if (s != HPL_OK) return s;
                 CK(c, cudaEventRecord(c->ev_panel[bn], c->s_la));
             }
@@ -700,7 +704,7 @@ hpl_status hpl_factor(hpl_ctx *c)
             if (s != HPL_OK) return s;
             if (E) CK(c, cudaEventRecord(E[5], c->s_la));
             if (has_next) {
-                s = fact_panel(c, c->s_la, j + 1, bn);
+                s = fact_panel(c, c->s_la, j + 1, bn, E ? E[7] : nullptr, E ? E[8] : nullptr);
                 if (s != HPL_OK) return s;
             }
             if (E) CK(c, cudaEventRecord(E[6], c->s_la));
@@ -714,11 +718,13 @@ hpl_status hpl_factor(hpl_ctx *c)
     c->launches = g_launches.load() - l0;
     c->factor_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
     c->timeline.clear();
+    c->fact_detail.clear();
     c->dgemm_ms = 0;
     if (c->timing) {
         c->timeline.reserve(6 * nblk);
+        c->fact_detail.reserve(3 * nblk);
         for (int64_t j = 0; j < nblk; ++j) {
-            cudaEvent_t *E = &c->tev[7 * j];
+            cudaEvent_t *E = &c->tev[10 * j];
             const double rest_dg = ev_ms(E[2], E[3]);
             c->timeline.push_back(c->lookahead ? ev_ms(E[5], E[6]) : ev_ms(E[5], E[6]));
             c->timeline.push_back(ev_ms(E[4], E[5]));
@@ -727,6 +733,10 @@ hpl_status hpl_factor(hpl_ctx *c)
             c->timeline.push_back(ev_ms(E[1], E[2]));
             c->timeline.push_back(rest_dg);
             c->dgemm_ms += rest_dg;
+            const bool nx = j + 1 < nblk;
+            c->fact_detail.push_back(nx ? ev_ms(E[5], E[7]) : 0.0);
+            c->fact_detail.push_back(nx ? ev_ms(E[7], E[8]) : 0.0);
+            c->fact_detail.push_back(nx ? ev_ms(E[8], E[6]) : 0.0);
         }
     }
     if (c->dist) {
@@ -771,14 +781,18 @@ hpl_status hpl_solve(hpl_ctx *c, double *x_host)
             const int rb = (int)(bb % c->P), qb = (int)(bb % c->Q);
             if (c->myrow == rb) {
                 const int64_t lr0 = lrows_before(c, r0);
-                CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda, lcols_before(c, r1),
-                                 lcN, c->NB, c->Q, c->mycol, c->x, lcy, c->tbuf));
+                // every rank of the process row uses the same split count
+                // (a function of the global sizes) so the all-reduce lines up
+                const int S = bs_splits(nb, 0, cdiv(cdiv(N - r1, c->NB), c->Q) * c->NB, c->NB);
+                CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda,
+                                       lcols_before(c, r1), lcN, c->NB, c->Q, c->mycol, c->x,
+                                       lcy, c->tbuf, S));
                 if (c->Q > 1)
-                    NK(c, ncclAllReduce(c->tbuf, c->tbuf, nb, ncclDouble, ncclSum, c->row_comm,
-                                        c->s_la));
+                    NK(c, ncclAllReduce(c->tbuf, c->tbuf, (size_t)S * nb, ncclDouble, ncclSum,
+                                        c->row_comm, c->s_la));
                 if (c->mycol == qb)
                     CK(c, bs_diag(c->s_la, nb, c->A + lr0 * c->lda + lcols_before(c, r0), c->lda,
-                                  c->tbuf, c->x + r0));
+                                  c->tbuf, S, c->x + r0));
             }
             if (c->dist)
                 NK(c, ncclBroadcast(c->x + r0, c->x + r0, nb, ncclDouble, rb + qb * c->P,
@@ -886,6 +900,14 @@ int64_t hpl_get_timeline(const hpl_ctx *c, double *t, int64_t cap)
     if (!c || !t) return 0;
     const int64_t n = std::min<int64_t>(cap, (int64_t)c->timeline.size() / 6);
     std::memcpy(t, c->timeline.data(), sizeof(double) * 6 * n);
+    return n;
+}
+
+int64_t hpl_get_fact_detail(const hpl_ctx *c, double *t, int64_t cap)
+{
+    if (!c || !t) return 0;
+    const int64_t n = std::min<int64_t>(cap, (int64_t)c->fact_detail.size() / 3);
+    std::memcpy(t, c->fact_detail.data(), sizeof(double) * 3 * n);
     return n;
 }
 

@@ -139,13 +139,16 @@ cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, c
 // Single-matrix back solve (y = column N of U's rows): hplk_back_solve.
 cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,
                        const double *y, int64_t ystride, double *x, double *tbuf);
-// partial[r] = sum_{lc_lo <= c < lc_hi} Urows[r][c] x[gcol(c)] - (lcy >= 0 ? Urows[r][lcy] : 0)
+// partial[s][r] (s < S, nb apart): the sum over the s-th share of the local
+// NB-blocks of Urows[r][c] x[gcol(c)], lc_lo <= c < lc_hi, minus Urows[r][lcy]
+// in share 0 when lcy >= 0.  S <= 16 (bs_splits suggests one); partial holds S * nb doubles.
+int bs_splits(int nb, int64_t lc_lo, int64_t lc_hi, int NB);
 cudaError_t bs_partial(cudaStream_t st, int nb, const double *Urows, int64_t ldu, int64_t lc_lo,
                        int64_t lc_hi, int NB, int Q, int mycol, const double *x, int64_t lcy,
-                       double *partial);
-// xb = U_bb^{-1} (-partial)
+                       double *partial, int S);
+// xb = U_bb^{-1} (-sum_s partial[s])
 cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
-                    const double *partial, double *xb);
+                    const double *partial, int S, double *xb);
 // Residual of the seeded system: per-rank partial sums (local rows x local
 // columns), then (after the caller's all-reduce over the process row) the
 // norms into out4 = {rinf, anorm, xnorm, bnorm} (max over local rows).

@@ -309,41 +309,38 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         const long long l = dp.lrL0 + (r - jbp);
         return ((l / dp.NB) * dp.P + dp.myrow) * dp.NB + l % dp.NB;
     };
+    // Panel rows are ordered like their global rows (T = block row j first,
+    // then this process's rows below it in block-cyclic order, a monotone
+    // map), so ties are broken on the panel row and the global row is formed
+    // once per CTA instead of per element.  T rows are candidates on the
+    // owner of block row j only.
+    double bv = -1.0;
+    long long br = LLONG_MAX;
+    for (int r = max(rbeg, k0) + threadIdx.x; r < rend; r += FACT_THREADS) {
+        if (r < jbp && !dp.is_prow) continue;
+        const double v = fabs(Pn[(int64_t)k0 * ldp + r]);
+        if (better(v, r, bv, br)) { bv = v; br = r; }
+    }
     for (int kk = 0; kk < w; ++kk) {
         const int kc = k0 + kk;
         const unsigned long long seq = seq0 + kk + 1;
         const int par = (int)(seq & 1);
         double *rec = cand + (size_t)(kk & 1) * (MAX_CTAS + 1) * REC;
-        // ---- 1. local candidates (T rows count on the owner of block row j only)
-        double bv = -1.0;
-        long long bg = LLONG_MAX;
-        int br = -1;
-        const double *colk = Pn + (int64_t)kc * ldp;
-        for (int r = max(rbeg, kc) + threadIdx.x; r < rend; r += FACT_THREADS) {
-            if (r < jbp && !dp.is_prow) continue;
-            const double v = fabs(colk[r]);
-            const long long g = grow(r);
-            if (better(v, g, bv, bg)) { bv = v; bg = g; br = r; }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const long long og = __shfl_xor_sync(0xffffffffu, bg, o);
-            const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-            if (better(ov, og, bv, bg)) { bv = ov; bg = og; br = orr; }
-        }
-        if ((threadIdx.x & 31) == 0) {
-            s_v[threadIdx.x >> 5] = bv; s_g[threadIdx.x >> 5] = bg; s_r[threadIdx.x >> 5] = br;
-        }
+        // ---- 1. this CTA's candidate (formed during the previous column's update)
+        long long bg;
+        warp_argmax(bv, br);
+        if ((threadIdx.x & 31) == 0) { s_v[threadIdx.x >> 5] = bv; s_g[threadIdx.x >> 5] = br; }
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int q = 1; q < FACT_THREADS / 32; ++q)
-                if (better(s_v[q], s_g[q], bv, bg)) { bv = s_v[q]; bg = s_g[q]; br = s_r[q]; }
+                if (better(s_v[q], s_g[q], bv, br)) { bv = s_v[q]; br = s_g[q]; }
+            bg = br != LLONG_MAX ? grow((int)br) : LLONG_MAX;
             double *myrec = rec + (size_t)blockIdx.x * REC;
             myrec[0] = bv;
             myrec[1] = __longlong_as_double(bg);
-            myrec[2] = __longlong_as_double((long long)br);
+            myrec[2] = __longlong_as_double(br != LLONG_MAX ? br : -1ll);
         }
+        int brr;
         __threadfence();
         grid_barrier(bar, G);
 
@@ -351,27 +348,27 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         // local "winner ready" flag instead of a second grid barrier.
         if (blockIdx.x == 0) {
             if (threadIdx.x < 32) {
-                bv = -1.0; bg = LLONG_MAX; br = -1;
+                bv = -1.0; bg = LLONG_MAX; brr = -1;
                 for (unsigned c = threadIdx.x; c < G; c += 32) {
                     const double v = __ldcg(rec + (size_t)c * REC);
                     const long long g = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
                     const int r = (int)__double_as_longlong(__ldcg(rec + (size_t)c * REC + 2));
-                    if (g != LLONG_MAX && better(v, g, bv, bg)) { bv = v; bg = g; br = r; }
+                    if (g != LLONG_MAX && better(v, g, bv, bg)) { bv = v; bg = g; brr = r; }
                 }
 #pragma unroll
                 for (int o = 16; o; o >>= 1) {
                     const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
                     const long long og = __shfl_xor_sync(0xffffffffu, bg, o);
-                    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-                    if (better(ov, og, bv, bg)) { bv = ov; bg = og; br = orr; }
+                    const int orr = __shfl_xor_sync(0xffffffffu, brr, o);
+                    if (better(ov, og, bv, bg)) { bv = ov; bg = og; brr = orr; }
                 }
-                if (threadIdx.x == 0) { s_v[0] = bv; s_g[0] = bg; s_r[0] = br; }
+                if (threadIdx.x == 0) { s_v[0] = bv; s_g[0] = bg; s_r[0] = brr; }
             }
             __syncthreads();
-            bv = s_v[0]; bg = s_g[0]; br = s_r[0];
+            bv = s_v[0]; bg = s_g[0]; brr = s_r[0];
             const size_t slot = ((size_t)par * ex.P + ex.myrow) * ex.recd;
             for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
-                const double pv = br >= 0 ? __ldcg(Pn + (int64_t)c * ldp + br) : 0.0;
+                const double pv = brr >= 0 ? __ldcg(Pn + (int64_t)c * ldp + brr) : 0.0;
                 for (int p = 0; p < ex.P; ++p) ex.rec[p][slot + 2 + c] = pv;
                 tsnap[c] = __ldcg(Pn + (int64_t)c * ldp + kc);
             }
@@ -448,9 +445,15 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
             if (piv == 0.0) atomicMin(info, (unsigned long long)(dp.j0 + kc));
         }
         __syncthreads();
-        // ---- 6. scale column kc and rank-1 update of the leaf columns (own rows > kc)
-        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += FACT_THREADS)
-            leaf_row_update(Pn, ldp, k0, w, kk, r, piv, s_pay + k0);
+        // ---- 6. scale column kc and rank-1 update of the leaf columns (own
+        // rows > kc); the next column's local candidate on the way
+        bv = -1.0;
+        br = LLONG_MAX;
+        const bool more = kk + 1 < w;
+        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += FACT_THREADS) {
+            const double nv = leaf_row_update(Pn, ldp, k0, w, kk, r, piv, s_pay + k0);
+            if (more && (r >= jbp || dp.is_prow) && better(nv, r, bv, br)) { bv = nv; br = r; }
+        }
         __syncthreads();
     }
 }

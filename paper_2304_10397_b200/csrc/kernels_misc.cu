@@ -218,60 +218,165 @@ cudaError_t trsm_cols(cudaStream_t st, int64_t k, int64_t ncols, const double *L
 //   partial[r] = sum_{local c : r1 <= gcol(c) < N} U[r][c] x[gcol(c)]  -  y[r] (y owner only)
 //   (summed over the process row), then x_b = U_bb^{-1} (-partial) on the
 //   owner of block column b.
-__global__ void bs_partial_kernel(const double *__restrict__ U, int64_t ldu, int64_t lc_lo,
-                                  int64_t lc_hi, int NB, int Q, int mycol,
-                                  const double *__restrict__ x, int64_t lcy, double *partial)
+// HBM-bound: every element of U is read once over the solve.  The partial
+// sums of one block row are split over S CTAs per row (grid nb x S, S whole
+// local NB-blocks each) so ~8 CTAs per SM stream U with 16-B loads; each
+// thread walks its pair offset through the local blocks, so the global
+// column needs no division.  The S partials are summed in a fixed order by
+// the diagonal kernel (deterministic).
+constexpr int BS_THREADS = 256;
+constexpr int BS_MAXSPLIT = 16;
+
+__global__ void __launch_bounds__(BS_THREADS)
+bs_partial_kernel(const double *__restrict__ U, int64_t ldu, int64_t lc_lo, int64_t lc_hi,
+                  int NB, int Q, int mycol, const double *__restrict__ x, int64_t lcy,
+                  double *partial, int nb, int64_t blocks_per_split, int vec)
 {
     const double *u = U + (int64_t)blockIdx.x * ldu;
-    double s = 0.0;
-    for (int64_t c = lc_lo + threadIdx.x; c < lc_hi; c += blockDim.x)
-        s += u[c] * x[l2g(c, NB, Q, mycol)];
-    __shared__ double red[32];
+    const int64_t lb_first = lc_lo / NB;
+    const int64_t lb0 = lb_first + (int64_t)blockIdx.y * blocks_per_split;
+    const int64_t lb1 = min(lb0 + blocks_per_split, (lc_hi + NB - 1) / NB);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 4
+    for (int64_t lb = lb0; lb < lb1; ++lb) {
+        const int64_t cb = lb * NB, gb = (lb * Q + mycol) * NB;
+        for (int o = 2 * threadIdx.x; o < NB; o += 2 * BS_THREADS) {
+            const int64_t c = cb + o;
+            if (vec && c >= lc_lo && c + 1 < lc_hi) {
+                const double2 uv = *reinterpret_cast<const double2 *>(u + c);
+                const double2 xv = *reinterpret_cast<const double2 *>(x + gb + o);
+                s0 = fma(uv.x, xv.x, s0);
+                s1 = fma(uv.y, xv.y, s1);
+            } else {
+                if (c >= lc_lo && c < lc_hi) s0 = fma(u[c], x[gb + o], s0);
+                if (o + 1 < NB && c + 1 >= lc_lo && c + 1 < lc_hi)
+                    s1 = fma(u[c + 1], x[gb + o + 1], s1);
+            }
+        }
+    }
+    double s = s0 + s1;
+    __shared__ double red[BS_THREADS / 32];
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x < 32) {
-        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        s = threadIdx.x < (BS_THREADS >> 5) ? red[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) partial[blockIdx.x] = s - (lcy >= 0 ? u[lcy] : 0.0);
+        if (threadIdx.x == 0)
+            partial[(int64_t)blockIdx.y * nb + blockIdx.x] =
+                s - (blockIdx.y == 0 && lcy >= 0 ? u[lcy] : 0.0);
     }
 }
 
-constexpr int BS_MAXB = 1024;
 // x[r0 + r] for r < nb from U_bb (rows of U starting at the block, columns
-// starting at the block's local column) and t = -partial.
-__global__ void __launch_bounds__(BS_MAXB)
+// starting at the block's local column) and t = -sum_s partial[s][r].
+// Blocked: 64-row sub-blocks from the bottom; each is staged in shared memory
+// with coalesced row loads, solved by one warp (two rows per lane, shuffles),
+// then the rows above are updated by a warp per row (coalesced 512-B reads).
+constexpr int BS_MAXB = 1024;
+constexpr int BS_SUB = 64;
+constexpr int BS_DIAG_THREADS = 512;
+
+__global__ void __launch_bounds__(BS_DIAG_THREADS)
 bs_diag_kernel(int nb, const double *__restrict__ Ubb, int64_t ldu,
-               const double *__restrict__ partial, double *xb)
+               const double *__restrict__ partial, int S, double *xb)
 {
-    __shared__ double xs[BS_MAXB];
-    const int r = threadIdx.x;
-    double acc = r < nb ? -partial[r] : 0.0;
-    const double *urow = Ubb + (int64_t)r * ldu;
-    for (int i = nb - 1; i >= 0; --i) {
-        if (r == i) xs[i] = acc / urow[i];
-        __syncthreads();
-        if (r < i) acc -= urow[i] * xs[i];
+    __shared__ double acc[BS_MAXB];
+    __shared__ double T[BS_SUB][BS_SUB + 1];
+    __shared__ double rinv[BS_SUB];
+    __shared__ double xs[BS_SUB];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = BS_DIAG_THREADS / 32;
+    for (int r = tid; r < nb; r += BS_DIAG_THREADS) {
+        double t = 0.0;
+        for (int s = 0; s < S; ++s) t += partial[(int64_t)s * nb + r];
+        acc[r] = -t;
     }
-    if (r < nb) xb[r] = xs[r];
+    const int nsub = (nb + BS_SUB - 1) / BS_SUB;
+    for (int kb = nsub - 1; kb >= 0; --kb) {
+        const int k0 = kb * BS_SUB, kn = min(BS_SUB, nb - k0);
+        for (int e = tid; e < BS_SUB * BS_SUB; e += BS_DIAG_THREADS) {
+            const int i = e / BS_SUB, j = e % BS_SUB;
+            T[i][j] = (i < kn && j < kn) ? Ubb[(int64_t)(k0 + i) * ldu + k0 + j] : 0.0;
+        }
+        __syncthreads();
+        if (tid < kn) rinv[tid] = 1.0 / T[tid][tid];
+        __syncthreads();
+        if (warp == 0) {
+            // rows lane and lane+32 of the sub-block; one shuffle + FMA per step
+            double a0 = lane < kn ? acc[k0 + lane] : 0.0;
+            double a1 = lane + 32 < kn ? acc[k0 + lane + 32] : 0.0;
+            for (int i = kn - 1; i >= 0; --i) {
+                const double t0 = T[lane][i], t1 = T[lane + 32][i], ri = rinv[i];
+                const double own = i < 32 ? a0 : a1;
+                const double xi = __shfl_sync(0xffffffffu, own, i & 31) * ri;
+                if (lane == 0) xs[i] = xi;
+                if (lane < i) a0 = fma(-t0, xi, a0);
+                if (lane + 32 < i) a1 = fma(-t1, xi, a1);
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < kn; i += BS_DIAG_THREADS) xb[k0 + i] = xs[i];
+        // rows above the sub-block: acc[r] -= U[r][k0:k0+kn] . xs, a warp per
+        // row, four rows' loads in flight per warp
+        const double xa = lane < kn ? xs[lane] : 0.0, xc = lane + 32 < kn ? xs[lane + 32] : 0.0;
+        for (int r0 = warp * 4; r0 < k0; r0 += NW * 4) {
+            double t[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = r0 + q;
+                const double *ur = Ubb + (int64_t)r * ldu + k0;
+                t[q] = 0.0;
+                if (r < k0) {
+                    if (lane < kn) t[q] = ur[lane] * xa;
+                    if (lane + 32 < kn) t[q] = fma(ur[lane + 32], xc, t[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double v = t[q];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && r0 + q < k0) acc[r0 + q] -= v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int bs_splits(int nb, int64_t lc_lo, int64_t lc_hi, int NB)
+{
+    if (lc_hi <= lc_lo || nb <= 0) return 1;
+    const int64_t nlb = (lc_hi + NB - 1) / NB - lc_lo / NB;
+    const int64_t want = cdiv((int64_t)148 * 8, nb);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, BS_MAXSPLIT), nlb));
 }
 
 cudaError_t bs_partial(cudaStream_t st, int nb, const double *Urows, int64_t ldu, int64_t lc_lo,
                        int64_t lc_hi, int NB, int Q, int mycol, const double *x, int64_t lcy,
-                       double *partial)
+                       double *partial, int S)
 {
     if (nb <= 0) return cudaSuccess;
-    bs_partial_kernel<<<nb, 256, 0, st>>>(Urows, ldu, lc_lo, lc_hi, NB, Q, mycol, x, lcy, partial);
+    if (S < 1 || S > BS_MAXSPLIT) return cudaErrorInvalidValue;
+    const int64_t nlb = lc_hi > lc_lo ? (lc_hi + NB - 1) / NB - lc_lo / NB : 0;
+    const int64_t bps = nlb > 0 ? cdiv(nlb, S) : 0;
+    // 16-B loads need even NB (so every pair stays inside one block and x
+    // pairs are aligned), even ldu and 16-B aligned bases
+    const int vec = (NB % 2 == 0 && ldu % 2 == 0 && (reinterpret_cast<uintptr_t>(Urows) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0)
+                        ? 1
+                        : 0;
+    bs_partial_kernel<<<dim3(nb, S), BS_THREADS, 0, st>>>(Urows, ldu, lc_lo, lc_hi, NB, Q, mycol,
+                                                          x, lcy, partial, nb, bps, vec);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
-                    const double *partial, double *xb)
+                    const double *partial, int S, double *xb)
 {
     if (nb <= 0) return cudaSuccess;
     if (nb > BS_MAXB) return cudaErrorInvalidValue;
-    bs_diag_kernel<<<1, ((nb + 31) / 32) * 32, 0, st>>>(nb, Ubb, ldu, partial, xb);
+    bs_diag_kernel<<<1, BS_DIAG_THREADS, 0, st>>>(nb, Ubb, ldu, partial, S, xb);
     count_launch();
     return cudaGetLastError();
 }
@@ -287,8 +392,9 @@ cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int6
     for (int64_t b = nblk - 1; b >= 0; --b) {
         const int64_t r0 = b * NB, r1 = std::min<int64_t>(N, r0 + NB);
         const int nb = (int)(r1 - r0);
-        HPL_CUDA_TRY(bs_partial(st, nb, U + r0 * ldu, ldu, r1, N, NB, 1, 0, x, lcy, tbuf));
-        HPL_CUDA_TRY(bs_diag(st, nb, U + r0 * ldu + r0, ldu, tbuf, x + r0));
+        const int S = bs_splits(nb, r1, N, NB);
+        HPL_CUDA_TRY(bs_partial(st, nb, U + r0 * ldu, ldu, r1, N, NB, 1, 0, x, lcy, tbuf, S));
+        HPL_CUDA_TRY(bs_diag(st, nb, U + r0 * ldu + r0, ldu, tbuf, S, x + r0));
     }
     return cudaGetLastError();
 }

@@ -146,6 +146,13 @@ def hpl_get_timeline(ctx: Ctx, cap: int = 1 << 16) -> np.ndarray:
     return buf[:n]
 
 
+def hpl_get_fact_detail(ctx: Ctx, cap: int = 1 << 16) -> np.ndarray:
+    """[wait, fact_local, lbcast_plan] ms per iteration (see include/hpl.h)."""
+    buf = np.zeros((cap, 3), dtype=np.float64)
+    n = lib.hpl_get_fact_detail(ctx.h, ptr(buf), cap)
+    return buf[:n]
+
+
 def hpl_set_timing(ctx: Ctx, enable: bool = True) -> None:
     ctx.check(lib.hpl_set_timing(ctx.h, 1 if enable else 0))
 

@@ -46,7 +46,10 @@ class IterationTrace:
 
 
 def traces_from_timeline(tl) -> List[IterationTrace]:
-    tl = np.asarray(tl, dtype=np.float64).reshape(-1, 6)
+    tl = np.asarray(tl, dtype=np.float64)
+    if tl.ndim == 2 and tl.shape[1] > 6:
+        tl = tl[:, :6]  # extra columns (fact breakdown) are not phases of the model
+    tl = tl.reshape(-1, 6)
     return [IterationTrace(j, *map(float, row)) for j, row in enumerate(tl)]
 
 

@@ -137,7 +137,8 @@ def test_laswp_identity_moves_nothing(H):
 
 
 # ------------------------------------------------------------------ a10 back solve
-@pytest.mark.parametrize("N,NB", [(300, 64), (1000, 256), (77, 32), (512, 512)])
+@pytest.mark.parametrize("N,NB", [(300, 64), (1000, 256), (77, 32), (512, 512), (4000, 128),
+                                  (301, 33), (2050, 1024), (3000, 2)])
 def test_back_solve_vs_oracle(H, N, NB):
     Uu = upper_well_conditioned(N, seed=N)
     y = np.random.default_rng(N + 1).uniform(-1, 1, N)

@@ -56,18 +56,25 @@ def main():
     tm = H.hpl_last_timing(ctx)
     if timeline:
         tl = H.hpl_get_timeline(ctx)
+        fd = H.hpl_get_fact_detail(ctx)
         fact, la_, rest, lsw, trsm, dg = tl.T
         summ = dict(rank=rank, factor_ms=round(tm["factor_ms"], 1), sum_fact=round(fact.sum(), 1),
                     sum_la=round(la_.sum(), 1), sum_rest=round(rest.sum(), 1),
                     sum_rs=round(lsw.sum(), 1), sum_trsm=round(trsm.sum(), 1),
                     sum_dgemm=round(dg.sum(), 1),
                     dgemm_tflops=round(tm["dgemm_flop"] / max(tm["dgemm_ms"], 1e-9) / 1e9, 2),
-                    fact_iter0=round(float(fact[0]), 2), rest_iter0=round(float(rest[0]), 2))
+                    fact_iter0=round(float(fact[0]), 2), rest_iter0=round(float(rest[0]), 2),
+                    sum_fact_wait=round(float(fd[:, 0].sum()), 1),
+                    sum_fact_local=round(float(fd[:, 1].sum()), 1),
+                    sum_lbcast_plan=round(float(fd[:, 2].sum()), 1),
+                    fact_local_iter0=round(float(fd[0, 1]), 2),
+                    lbcast_plan_iter0=round(float(fd[0, 2]), 2))
         print(json.dumps(summ), flush=True)
         for a in sys.argv[1:]:
             if a.startswith("--timeline-out="):
-                np.savetxt(f"{a.split('=', 1)[1]}_r{rank}.csv", tl, delimiter=",", fmt="%.4f",
-                           header="fact,la_update,rest_update,rest_rs,rest_trsm,rest_dgemm")
+                np.savetxt(f"{a.split('=', 1)[1]}_r{rank}.csv", np.hstack([tl, fd]), delimiter=",",
+                           fmt="%.4f", header="fact,la_update,rest_update,rest_rs,rest_trsm,"
+                           "rest_dgemm,fact_wait,fact_local,lbcast_plan")
     ipiv = H.hpl_get_ipiv(ctx)
     r = H.hpl_residual(ctx)
     H.hpl_free(ctx)

@@ -2,11 +2,13 @@
 [fact, la_update, rest_update, rest_laswp, rest_trsm, rest_dgemm] ms per
 iteration; prints a summary and writes the CSV (PAPER.md Fig. iteration analog)."""
 import json
+import os
 import sys
 
 import numpy as np
 
-import paper_2304_10397_b200 as H
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2304_10397_b200 as H  # noqa: E402
 
 N, NB = int(sys.argv[1]), int(sys.argv[2])
 rest = sys.argv[3:]
@@ -23,6 +25,7 @@ H.hpl_factor(ctx)
 H.hpl_solve(ctx, want_x=False)
 t = H.hpl_last_timing(ctx)
 tl = H.hpl_get_timeline(ctx)
+fd = H.hpl_get_fact_detail(ctx)
 r = H.hpl_residual(ctx)
 H.hpl_free(ctx)
 fact, la, rest, lsw, trsm, dg = tl.T
@@ -32,8 +35,11 @@ s = dict(N=N, NB=NB, opts=opts, factor_ms=t["factor_ms"], solve_ms=t["solve_ms"]
          sum_trsm=trsm.sum(), sum_dgemm=dg.sum(), sum_crit=crit.sum(),
          exposed_iters=int(np.sum(la + fact > rest)),
          exposed_ms=float(np.sum(np.maximum(0, la + fact - rest))),
-         dgemm_tflops=t["dgemm_flop"] / (t["dgemm_ms"] * 1e-3) / 1e12)
-print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in s.items()}))
+         dgemm_tflops=t["dgemm_flop"] / (t["dgemm_ms"] * 1e-3) / 1e12,
+         sum_fact_wait=float(fd[:, 0].sum()), sum_fact_local=float(fd[:, 1].sum()),
+         sum_lbcast_plan=float(fd[:, 2].sum()))
+print(json.dumps({k: (v if k == "resid" else round(v, 3) if isinstance(v, float) else v)
+                  for k, v in s.items()}))
 if out:
     np.savetxt(out, tl, delimiter=",", header="fact,la_update,rest_update,rest_laswp,rest_trsm,rest_dgemm",
                fmt="%.4f")
