@@ -80,6 +80,7 @@ struct hpl_ctx {
     int nbmin = 16;
     bool leaf_auto = true;           // adaptive leaf grid (fact_panel)
     int leaf_few_ctas = 8;
+    int leaf_warp = 0;               // >0: hidden FACT uses up to this many one-warp leaf CTAs
     double leaf_hide_ms = 60.0;
     bool timing = false;
     std::vector<cudaEvent_t> tev;   // 7 events per iteration when timing
@@ -224,7 +225,9 @@ hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b, cudaEvent_t
         const int64_t j0 = j * c->NB, rows = c->mloc - lrows_before(c, j0);
         const int64_t ncols = c->nloc - lcols_before(c, j0);
         const double rest_ms = 2.0 * (double)rows * (double)ncols * c->NB / 35e12 * 1e3;
-        fact_set_leaf_ctas(rest_ms > c->leaf_hide_ms ? c->leaf_few_ctas : 0, 512);
+        const bool hide = rest_ms > c->leaf_hide_ms;
+        fact_set_leaf_ctas(hide ? c->leaf_few_ctas : 0, 512);
+        fact_set_leaf_warp_ctas(hide ? c->leaf_warp : 0);
     }
     if (c->mycol == (int)(j % c->Q)) {
         hpl_status s = fact_local(c, st, j, b);
@@ -928,7 +931,11 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     } else if (!strcmp(name, "gemm_cfg")) dgemm_set_default_cfg((int)value);
     else if (!strcmp(name, "gemm_tpc")) dgemm_set_tiles_per_cta((int)value);
     else if (!strcmp(name, "gemm_red")) dgemm_set_red_epilogue((int)value);
-    else if (!strcmp(name, "leaf_ctas")) { c->leaf_auto = false; fact_set_leaf_ctas((int)value, 0); }
+    else if (!strcmp(name, "leaf_ctas")) {
+        c->leaf_auto = false;
+        fact_set_leaf_warp_ctas(0);
+        fact_set_leaf_ctas((int)value, 0);
+    } else if (!strcmp(name, "leaf_warp")) { c->leaf_auto = true; c->leaf_warp = (int)value; }
     else if (!strcmp(name, "leaf_rows")) { c->leaf_auto = false; fact_set_leaf_ctas(-1, (int)value); }
     else if (!strcmp(name, "split")) c->split_pct = (int)value;
     else if (!strcmp(name, "early_next")) c->early_next = value != 0;

@@ -98,6 +98,9 @@ cudaError_t fact_work_alloc(FactWork *w);
 // Leaf grid size: min(max_ctas (0 = #SMs), ceil(rows / rows_per_cta)).  Fewer
 // CTAs leave more of each SM to the concurrent trailing DGEMM.
 void fact_set_leaf_ctas(int max_ctas, int rows_per_cta);
+// > 0: leaves run as one-warp CTAs (at most this many) that fit next to the
+// trailing DGEMM's CTAs; 0: the multi-warp leaf with fact_set_leaf_ctas' grid
+void fact_set_leaf_warp_ctas(int ctas);
 // Pivot winner among n candidates (max |v|, ties -> smallest row), as the FACT reduces.
 cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,
                        int64_t *winner);

@@ -93,7 +93,12 @@ __device__ __forceinline__ double leaf_row_update(double *P, int64_t ldp, int k0
 // One grid barrier per column; the next column's local pivot candidate is
 // formed during the current column's update, so a column costs the barrier
 // plus about three L2 round trips.
-__global__ void __launch_bounds__(FACT_THREADS)
+// NT = 256: the leaf on its own SMs (FACT on the critical path).  NT = 32:
+// one warp per CTA, at most 128 registers, so a leaf CTA fits on an SM next
+// to three trailing-DGEMM CTAs (3 x 160 threads x 128 registers + 32 x 128 =
+// the 64 K register file) and takes no DGEMM slot while FACT hides behind it.
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1)
 leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, double *cand,
                  unsigned *bar, unsigned long long *info, long long goff)
 {
@@ -102,9 +107,9 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
     const int chunk = (nrows + (int)G - 1) / (int)G;
     const int rbeg = k0 + (int)blockIdx.x * chunk;
     const int rend = min(m, rbeg + chunk);
-    __shared__ double s_v[FACT_THREADS / 32];
-    __shared__ long long s_r[FACT_THREADS / 32];
-    __shared__ int s_c[FACT_THREADS / 32];
+    __shared__ double s_v[NT / 32];
+    __shared__ long long s_r[NT / 32];
+    __shared__ int s_c[NT / 32];
     __shared__ double s_prow[LEAF_MAX], s_rowk[LEAF_MAX];
     __shared__ long long s_p;
     __shared__ double s_piv;
@@ -112,7 +117,7 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
     // local candidate for the first leaf column
     double bv = -1.0;
     long long br = LLONG_MAX;
-    for (int i = max(rbeg, k0) + threadIdx.x; i < rend; i += FACT_THREADS) {
+    for (int i = max(rbeg, k0) + threadIdx.x; i < rend; i += NT) {
         const double v = fabs(P[(int64_t)k0 * ldp + i]);
         if (better(v, i, bv, br)) { bv = v; br = i; }
     }
@@ -124,8 +129,8 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
         if ((threadIdx.x & 31) == 0) { s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; }
         __syncthreads();
         if (threadIdx.x < 32) {
-            bv = threadIdx.x < FACT_THREADS / 32 ? s_v[threadIdx.x] : -1.0;
-            br = threadIdx.x < FACT_THREADS / 32 ? s_r[threadIdx.x] : LLONG_MAX;
+            bv = threadIdx.x < NT / 32 ? s_v[threadIdx.x] : -1.0;
+            br = threadIdx.x < NT / 32 ? s_r[threadIdx.x] : LLONG_MAX;
             warp_argmax(bv, br);
             double *myrec = rec + (size_t)blockIdx.x * REC;
             if (threadIdx.x == 0) {
@@ -144,7 +149,7 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
         bv = -1.0;
         br = LLONG_MAX;
         int bc = -1;
-        for (int c = threadIdx.x; c < (int)G; c += FACT_THREADS) {
+        for (int c = threadIdx.x; c < (int)G; c += NT) {
             // other CTAs wrote these: read through L2 (L1 is not coherent)
             const double v = __ldcg(rec + (size_t)c * REC);
             const long long r = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
@@ -162,7 +167,7 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
         }
         __syncthreads();
         if (threadIdx.x < 32) {
-            const bool ok = threadIdx.x < FACT_THREADS / 32;
+            const bool ok = threadIdx.x < NT / 32;
             bv = ok ? s_v[threadIdx.x] : -1.0;
             br = ok ? s_r[threadIdx.x] : LLONG_MAX;
             bc = ok ? s_c[threadIdx.x] : -1;
@@ -200,7 +205,7 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
         // ---- 4. scale + rank-1 update of own rows > kc; next column's candidate
         bv = -1.0;
         br = LLONG_MAX;
-        for (int i = max(rbeg, kc + 1) + threadIdx.x; i < rend; i += FACT_THREADS) {
+        for (int i = max(rbeg, kc + 1) + threadIdx.x; i < rend; i += NT) {
             const double nv = leaf_row_update(P, ldp, k0, w, kk, i, piv, s_prow);
             if (kk + 1 < w && better(nv, i, bv, br)) { bv = nv; br = i; }
         }
@@ -288,7 +293,8 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned l
 // grid barrier -> full-width swap on the owners -> rank-1 update of the leaf
 // columns.  The top block T is replicated on all P processes and updated
 // identically by each, so only the winner's payload crosses NVLink.
-__global__ void __launch_bounds__(FACT_THREADS)
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1)
 leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ipiv, double *cand,
                       double *win, double *tsnap, unsigned long long *winflag, unsigned *bar,
                       unsigned long long *info, DistPanel dp, DistExchange ex,
@@ -299,9 +305,9 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
     const int rbeg = (int)blockIdx.x * chunk;
     const int rend = min(m, rbeg + chunk);
     const int jbp = dp.jbp;
-    __shared__ double s_v[FACT_THREADS / 32];
-    __shared__ long long s_g[FACT_THREADS / 32];
-    __shared__ int s_r[FACT_THREADS / 32];
+    __shared__ double s_v[NT / 32];
+    __shared__ long long s_g[NT / 32];
+    __shared__ int s_r[NT / 32];
     __shared__ double s_pay[1024], s_ts[1024];
     __shared__ long long s_win;
     auto grow = [&](int r) -> long long {
@@ -316,7 +322,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
     // owner of block row j only.
     double bv = -1.0;
     long long br = LLONG_MAX;
-    for (int r = max(rbeg, k0) + threadIdx.x; r < rend; r += FACT_THREADS) {
+    for (int r = max(rbeg, k0) + threadIdx.x; r < rend; r += NT) {
         if (r < jbp && !dp.is_prow) continue;
         const double v = fabs(Pn[(int64_t)k0 * ldp + r]);
         if (better(v, r, bv, br)) { bv = v; br = r; }
@@ -332,7 +338,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         if ((threadIdx.x & 31) == 0) { s_v[threadIdx.x >> 5] = bv; s_g[threadIdx.x >> 5] = br; }
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int q = 1; q < FACT_THREADS / 32; ++q)
+            for (int q = 1; q < NT / 32; ++q)
                 if (better(s_v[q], s_g[q], bv, br)) { bv = s_v[q]; br = s_g[q]; }
             bg = br != LLONG_MAX ? grow((int)br) : LLONG_MAX;
             double *myrec = rec + (size_t)blockIdx.x * REC;
@@ -367,7 +373,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
             __syncthreads();
             bv = s_v[0]; bg = s_g[0]; brr = s_r[0];
             const size_t slot = ((size_t)par * ex.P + ex.myrow) * ex.recd;
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+            for (int c = threadIdx.x; c < jbp; c += NT) {
                 const double pv = brr >= 0 ? __ldcg(Pn + (int64_t)c * ldp + brr) : 0.0;
                 for (int p = 0; p < ex.P; ++p) ex.rec[p][slot + 2 + c] = pv;
                 tsnap[c] = __ldcg(Pn + (int64_t)c * ldp + kc);
@@ -401,7 +407,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
             }
             __syncthreads();
             const double *wr = ex.my_rec + ((size_t)par * ex.P + s_r[0]) * ex.recd;
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+            for (int c = threadIdx.x; c < jbp; c += NT) {
                 const double v = __ldcv(wr + 2 + c);
                 win[2 + c] = v;
                 s_pay[c] = v;
@@ -418,7 +424,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
                 }
             __syncthreads();
             if (threadIdx.x == 0) s_win = __double_as_longlong(__ldcg(win));
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) {
+            for (int c = threadIdx.x; c < jbp; c += NT) {
                 s_pay[c] = __ldcg(win + 2 + c);
                 s_ts[c] = __ldcg(tsnap + c);
             }
@@ -429,7 +435,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         const long long gw = s_win;
         const long long t = gw - dp.j0;
         if (kc >= rbeg && kc < rend)
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) Pn[(int64_t)c * ldp + kc] = s_pay[c];
+            for (int c = threadIdx.x; c < jbp; c += NT) Pn[(int64_t)c * ldp + kc] = s_pay[c];
         long long rswap = -1;
         if (t >= 0 && t < jbp) {
             if (t != kc) rswap = t;
@@ -438,7 +444,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
             rswap = jbp + (l - dp.lrL0);
         }
         if (rswap >= rbeg && rswap < rend)
-            for (int c = threadIdx.x; c < jbp; c += FACT_THREADS) Pn[(int64_t)c * ldp + rswap] = s_ts[c];
+            for (int c = threadIdx.x; c < jbp; c += NT) Pn[(int64_t)c * ldp + rswap] = s_ts[c];
         const double piv = s_pay[kc];
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ipiv[kc] = t;
@@ -450,7 +456,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         bv = -1.0;
         br = LLONG_MAX;
         const bool more = kk + 1 < w;
-        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += FACT_THREADS) {
+        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += NT) {
             const double nv = leaf_row_update(Pn, ldp, k0, w, kk, r, piv, s_pay + k0);
             if (more && (r >= jbp || dp.is_prow) && better(nv, r, bv, br)) { bv = nv; br = r; }
         }
@@ -461,6 +467,23 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
 int g_num_sms = 0;
 int g_leaf_max_ctas = 0;        // 0 = all SMs
 int g_leaf_rows_per_cta = 512;
+int g_leaf_warp_ctas = 0;       // > 0: one-warp CTAs (co-resident with the DGEMM), at most this many
+constexpr int WARP_LEAF_MIN_ROWS = 128;
+
+// grid of the next leaf launch: {CTAs, threads per CTA}
+void leaf_grid(int64_t rows, int max_ctas, int *G, int *NT)
+{
+    if (g_leaf_warp_ctas > 0) {
+        *NT = 32;
+        *G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, WARP_LEAF_MIN_ROWS)),
+                                    std::min(g_leaf_warp_ctas, max_ctas));
+        return;
+    }
+    const int gmax = g_leaf_max_ctas > 0 ? std::min(g_leaf_max_ctas, g_num_sms) : g_num_sms;
+    *NT = FACT_THREADS;
+    *G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, g_leaf_rows_per_cta)), gmax);
+    *G = std::min(*G, max_ctas);
+}
 
 cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
                         int64_t *ipiv, FactWork *wk, long long goff)
@@ -470,17 +493,16 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int 
         HPL_CUDA_TRY(cudaGetDevice(&dev));
         HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int64_t rows = m - k0;
-    const int gmax = g_leaf_max_ctas > 0 ? std::min(g_leaf_max_ctas, g_num_sms) : g_num_sms;
-    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, g_leaf_rows_per_cta)), gmax);
-    G = std::min(G, wk->max_ctas);
+    int G, NT;
+    leaf_grid(m - k0, wk->max_ctas, &G, &NT);
     int m_i = (int)m;
     int64_t ldp_ = ldp;
     int k0_ = k0, w_ = w;
     unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
     void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->bar, &info, &goff};
-    HPL_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)leaf_fact_kernel, dim3(G),
-                                             dim3(FACT_THREADS), args, 0, st));
+    const void *fn = NT == 32 ? (const void *)leaf_fact_kernel<32>
+                              : (const void *)leaf_fact_kernel<FACT_THREADS>;
+    HPL_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), args, 0, st));
     count_launch();
     if (w < 0) return cudaErrorInvalidValue;
     return cudaSuccess;
@@ -495,9 +517,8 @@ cudaError_t launch_leaf_dist(cudaStream_t st, int64_t m, double *P, int64_t ldp,
         HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     if (df->dp.jbp > 1024) return cudaErrorInvalidValue;
-    const int gmax = g_leaf_max_ctas > 0 ? std::min(g_leaf_max_ctas, g_num_sms) : g_num_sms;
-    int G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(m, g_leaf_rows_per_cta)), gmax);
-    G = std::min(G, wk->max_ctas);
+    int G, NT;
+    leaf_grid(m, wk->max_ctas, &G, &NT);
     int m_i = (int)m;
     int64_t ldp_ = ldp;
     int k0_ = k0, w_ = w;
@@ -506,8 +527,9 @@ cudaError_t launch_leaf_dist(cudaStream_t st, int64_t m, double *P, int64_t ldp,
     unsigned long long *winflag = reinterpret_cast<unsigned long long *>(wk->bar + 8);
     void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->win, &wk->tsnap,
                     &winflag, &wk->bar, &info, &df->dp, &df->ex, &seq0};
-    HPL_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)leaf_fact_dist_kernel, dim3(G),
-                                             dim3(FACT_THREADS), args, 0, st));
+    const void *fn = NT == 32 ? (const void *)leaf_fact_dist_kernel<32>
+                              : (const void *)leaf_fact_dist_kernel<FACT_THREADS>;
+    HPL_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), args, 0, st));
     *df->seq += (unsigned long long)w;
     count_launch();
     return cudaSuccess;
@@ -576,6 +598,8 @@ cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64
     count_launch();
     return cudaGetLastError();
 }
+
+void fact_set_leaf_warp_ctas(int ctas) { g_leaf_warp_ctas = ctas; }
 
 void fact_set_leaf_ctas(int max_ctas, int rows_per_cta)
 {

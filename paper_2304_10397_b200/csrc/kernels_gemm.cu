@@ -21,6 +21,7 @@
 //  - Tiles are rasterised in groups of GROUP_M m-tiles so the L panel and U
 //    block row of a wave stay L2-resident.
 #include "hpl_internal.cuh"
+#include <type_traits>
 #include <cuda.h>
 #include <mutex>
 
@@ -146,7 +147,7 @@ struct alignas(64) ParamPad {
     unsigned char b[64 * (SLOT + 1)];
 };
 
-template <class C, int SLOT>
+template <class C, int SLOT, bool RED>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
 dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
                  const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB)
@@ -304,7 +305,7 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
                 // row 2g: lo.c0 hi.c0 lo.c1 hi.c1 ; row 2g+1: lo.c2 hi.c2 lo.c3 hi.c3
                 const double v0 = acc[i][j][0][2 * h], v1 = acc[i][j][1][2 * h];
                 const double v2 = acc[i][j][0][2 * h + 1], v3 = acc[i][j][1][2 * h + 1];
-                if (p.red_epi && p.mode == GEMM_UPDATE) {
+                if (RED && p.mode == GEMM_UPDATE) {
                     // C + (-acc) performed at L2: one rounding, as C - acc; the
                     // warp does not wait for C (each element is touched once)
                     if (col + 0 < p.n) red_add(crow + col + 0, -v0);
@@ -398,19 +399,21 @@ int g_default_cfg = 2;
 int g_tiles_per_cta = 1;
 int g_red_epi = 0;
 
-template <class C, int SLOT>
+// The RED epilogue is a separate instantiation (default config only): a
+// runtime branch in the epilogue made the default kernel spill.
+template <class C, int SLOT, bool RED = false>
 cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
                         const GemmParams &p)
 {
     static bool attr_set = false;
     if (!attr_set) {
-        HPL_CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT>,
+        HPL_CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT, RED>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
     const long long grid = cdiv(p.ntiles, p.tiles_per_cta);
     ParamPad<SLOT> pad{};
-    dgemm_tma_kernel<C, SLOT><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
+    dgemm_tma_kernel<C, SLOT, RED><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
     count_launch();
     return cudaGetLastError();
 }
@@ -425,6 +428,10 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
     // several tiles per CTA only for large grids (short kernels keep one tile
     // per CTA so concurrent FACT kernels find free SM slots quickly)
     p.tiles_per_cta = p.ntiles >= 16 * 148 * C::MINB ? g_tiles_per_cta : 1;
+    if constexpr (std::is_same_v<C, CfgC>) {
+        if (p.red_epi && p.mode == GEMM_UPDATE && slot == 0)
+            return launch_slot<C, 0, true>(st, ma, mb, p);
+    }
     switch (slot) {
     case 1: return launch_slot<C, 1>(st, ma, mb, p);
     case 2: return launch_slot<C, 2>(st, ma, mb, p);

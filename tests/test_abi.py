@@ -66,3 +66,25 @@ def test_invalid_args_rejected_without_gpu_work():
     for args in [(0, 32, 1, 1), (100, 0, 1, 1), (100, 200, 1, 1), (100, 32, 2, 1)]:
         assert _lib.lib.hpl_init(*args, 1, ctypes.byref(h)) == 1  # HPL_ERR_ARG
         assert not h.value
+
+
+def test_hot_kernels_do_not_spill():
+    """The trailing-update DGEMM (default 64x64 config, every stream slot) and
+    the distributed leaf keep everything in registers: a local-memory stack
+    frame in them cost ~1.5 % of the HPL rate once (an epilogue branch)."""
+    lib = _build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", lib],
+                         capture_output=True, text=True).stdout
+    lines = out.splitlines()
+    hot = 0
+    for i, l in enumerate(lines):
+        if "Function" not in l:
+            continue
+        name = l
+        usage = lines[i + 1] if i + 1 < len(lines) else ""
+        if ("dgemm_tma_kernel" in name and "ILi64ELi64ELi32ELi32ELi4ELi3EEE" in name) or \
+                "leaf_fact_dist_kernel" in name:
+            hot += 1
+            m = re.search(r"STACK:(\d+)", usage)
+            assert m and int(m.group(1)) == 0, name + " " + usage
+    assert hot >= 4

@@ -194,6 +194,26 @@ def test_split_update_single_gpu_invariance(H):
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
 
 
+@pytest.mark.parametrize("opts", [{"leaf_warp": 148, "leaf_hide_ms": 0},
+                                  {"leaf_warp": 7, "leaf_hide_ms": 0},
+                                  {"leaf_ctas": 3}, {"leaf_ctas": 0}])
+def test_leaf_grid_invariance(H, opts):
+    """The leaf's grid (one-warp CTAs beside the DGEMM, few or all multi-warp
+    CTAs) only changes which CTA updates a row, never the arithmetic: pivots
+    equal the oracle's and x is bitwise that of the default grid."""
+    def run(o):
+        with H.hpl_init(3000, 128, 1, 1, 17) as ctx:
+            for k, v in o.items():
+                H.hpl_set_option(ctx, k, v)
+            H.hpl_factor(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+    xa, pa, _ = run({})
+    xb, pb, rb = run(opts)
+    o = oracle.run(3000, 17)
+    assert np.array_equal(pb, o["ipiv"]) and np.array_equal(pa, pb)
+    assert np.array_equal(xa, xb) and rb < 16
+
+
 def test_hpl_c1_vs_oracle(H):
     """BASELINE.json configs[1]: N=8192 NB=256 1x1."""
     N, NB, seed = 8192, 256, 42

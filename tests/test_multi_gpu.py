@@ -102,3 +102,13 @@ def test_split_update_schedule_invariance():
     a = _run(2, 3072, 128, 2, 1, ("--opt=split=0",))
     b = _run(2, 3072, 128, 2, 1, ("--opt=split=30",))
     assert a["ipiv_equal"] and b["ipiv_equal"] and a["resid"] < 16 and b["resid"] < 16
+
+
+@pytest.mark.parametrize("opts", [("--opt=leaf_warp=148", "--opt=leaf_hide_ms=0"),
+                                  ("--opt=leaf_warp=5", "--opt=leaf_hide_ms=0")])
+def test_2x1_warp_leaf(opts):
+    """Distributed leaf as one-warp CTAs (the grid used beside long DGEMMs)."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = _run(2, 3000, 128, 2, 1, opts)
+    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
