@@ -46,6 +46,24 @@ struct hpl_ctx {
     std::vector<void *> xpeer;
     DistExchange xch{};
     unsigned long long xseq = 0;
+    // P > 1 RS over peer memory (option rs_peer, default on): every process
+    // row's A and barrier flags, IPC-mapped inside the process column
+    bool rs_peer = true;
+    unsigned long long *rsflag = nullptr;
+    std::vector<void *> apeer, fpeer;
+    RsPeers rsp{};
+    unsigned long long rs_seq[3] = {0, 0, 0};
+    // Q > 1 LBCAST over peer memory (option lb_peer, default on): the panel
+    // buffers and LBCAST flags of every process column, IPC-mapped inside the
+    // process row.  lbflag[o] = last panel (+1) owner o has ready;
+    // lbflag[LB_DONE + q] = last panel (+1) of this owner that column q copied.
+    static constexpr int LB_DONE = 32;
+    bool lb_peer = true;
+    unsigned long long lb_base = 0, lb_next = 0;  // flag value of panel j = lb_base + j + 1
+    unsigned long long *lbflag = nullptr;
+    std::vector<void *> lbpeer;                 // opened handles (Q x (NBUF + 1))
+    std::vector<const double *> ppanel;         // [q * NBUF + b]: column q's panel[b]
+    std::vector<unsigned long long *> pflag;    // [q]: column q's lbflag
     double *rvec = nullptr, *avec = nullptr;   // residual partial sums (N each)
     // local storage
     int64_t mloc = 0, nloc = 0, lda = 0;
@@ -203,9 +221,31 @@ hpl_status lbcast_and_plan(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
 {
     const int64_t j0 = j * c->NB, jb = jb_of(c, j), ldpj = panel_ld(c, j);
     const int pcol = (int)(j % c->Q);
-    if (c->Q > 1)
+    const size_t pbytes = sizeof(double) * (size_t)((jb + 1) * ldpj);
+    if (c->Q > 1 && c->lb_peer) {
+        // owner: announce panel j; receivers: wait for it, pull it with the copy
+        // engine over NVLink (no SMs), tell the owner the buffer was read
+        FlagOp op{};
+        if (c->mycol == pcol) {
+            for (int q = 0; q < c->Q; ++q)
+                if (q != pcol) op.sig[op.nsig++] = c->pflag[q] + pcol;
+            op.sv = c->lb_base + (unsigned long long)j + 1;
+            CK(c, flag_op(st, op));
+        } else {
+            op.wt[op.nwait++] = c->lbflag + pcol;
+            op.wv = c->lb_base + (unsigned long long)j + 1;
+            CK(c, flag_op(st, op));
+            CK(c, cudaMemcpyAsync(c->panel[b], c->ppanel[pcol * hpl_ctx::NBUF + b], pbytes,
+                                  cudaMemcpyDeviceToDevice, st));
+            FlagOp done{};
+            done.sig[done.nsig++] = c->pflag[pcol] + hpl_ctx::LB_DONE + c->mycol;
+            done.sv = c->lb_base + (unsigned long long)j + 1;
+            CK(c, flag_op(st, done));
+        }
+    } else if (c->Q > 1) {
         NK(c, ncclBroadcast(c->panel[b], c->panel[b], (size_t)((jb + 1) * ldpj), ncclDouble, pcol,
                             c->row_comm, st));
+    }
     // the plan is in GLOBAL rows (P = 1: global == local)
     CK(c, pivot_plan(st, jb, j0, panel_ipiv(c, j, b), j0, c->gpiv + j0, c->src[b], c->disp[b],
                      c->ndisp[b]));
@@ -230,6 +270,15 @@ hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b, cudaEvent_t
         fact_set_leaf_warp_ctas(hide ? c->leaf_warp : 0);
     }
     if (c->mycol == (int)(j % c->Q)) {
+        if (c->Q > 1 && c->lb_peer && j >= c->Q) {
+            // panel[b] is about to be overwritten: every other column must have
+            // copied this column's previous panel (j - Q) (and so all earlier ones)
+            FlagOp op{};
+            for (int q = 0; q < c->Q; ++q)
+                if (q != c->mycol) op.wt[op.nwait++] = c->lbflag + hpl_ctx::LB_DONE + q;
+            op.wv = c->lb_base + (unsigned long long)(j - c->Q) + 1;
+            CK(c, flag_op(st, op));
+        }
         hpl_status s = fact_local(c, st, j, b);
         if (s != HPL_OK) return s;
     }
@@ -267,6 +316,20 @@ hpl_status rs_cols(hpl_ctx *c, cudaStream_t st, int64_t j, int b, int64_t c0, in
     const int64_t lr0 = lrows_before(c, j0);
     const int64_t ldub = round_up(n, 16);
     double *u = c->Ub[sec], *w = c->Wb[sec];
+    if (c->rs_peer) {
+        // peer memory: barrier (peers' columns are at iteration j), gather U and
+        // this process's W rows over NVLink, barrier (peers done reading), scatter
+        const unsigned long long v = ++c->rs_seq[sec];
+        CK(c, rs_barrier(st, c->rsp, 2 * sec, v));
+        CK(c, rs_gather_peer(st, jb, c->src[b], c->disp[b], c->ndisp[b], c->rsp, c->lda, c0, c1,
+                             u, ldub, w, ldub, j0, c->NB));
+        CK(c, rs_barrier(st, c->rsp, 2 * sec + 1, v));
+        CK(c, rs_scatter(st, c->disp[b], c->ndisp[b], w, ldub, j0, c->A, c->lda, c0, c1, c->NB,
+                         c->P, c->myrow));
+        out->u = u;
+        out->ldu = ldub;
+        return HPL_OK;
+    }
     CK(c, rs_pack(st, jb, c->src[b], c->A, c->lda, c0, c1, u, ldub, c->NB, c->P, c->myrow));
     if (c->myrow == prow_of(c, j))
         CK(c, cudaMemcpy2DAsync(w, ldub * 8, c->A + lr0 * c->lda + c0, c->lda * 8, n * 8, jb,
@@ -444,6 +507,11 @@ void release(hpl_ctx *c)
     cudaFree(c->Tbuf);
     for (int k = 0; k < 3; ++k) { cudaFree(c->Ub[k]); cudaFree(c->Wb[k]); }
     for (void *pp : c->xpeer) if (pp) cudaIpcCloseMemHandle(pp);
+    for (void *pp : c->apeer) if (pp) cudaIpcCloseMemHandle(pp);
+    for (void *pp : c->lbpeer) if (pp) cudaIpcCloseMemHandle(pp);
+    cudaFree(c->lbflag);
+    for (void *pp : c->fpeer) if (pp) cudaIpcCloseMemHandle(pp);
+    cudaFree(c->rsflag);
     cudaFree(c->xbuf);
     if (c->col_comm_tr) ncclCommDestroy(c->col_comm_tr);
     if (c->row_comm) ncclCommDestroy(c->row_comm);
@@ -472,24 +540,46 @@ hpl_status setup_exchange(hpl_ctx *c)
     const size_t bytes = rec_bytes + sizeof(unsigned long long) * 2 * P;
     CK(c, cudaMalloc(&c->xbuf, bytes));
     CK(c, cudaMemset(c->xbuf, 0, bytes));
-    cudaIpcMemHandle_t h;
-    CK(c, cudaIpcGetMemHandle(&h, c->xbuf));
+    const size_t fbytes = sizeof(unsigned long long) * RS_SLOTS * MAX_P;
+    CK(c, cudaMalloc(&c->rsflag, fbytes));
+    CK(c, cudaMemset(c->rsflag, 0, fbytes));
+    // three handles per process row: exchange area, local A, RS flags
+    cudaIpcMemHandle_t h[3];
+    CK(c, cudaIpcGetMemHandle(&h[0], c->xbuf));
+    CK(c, cudaIpcGetMemHandle(&h[1], c->A));
+    CK(c, cudaIpcGetMemHandle(&h[2], c->rsflag));
     char *dh = nullptr;
     CK(c, cudaMalloc(&dh, sizeof(h) * P));
-    CK(c, cudaMemcpy(dh + sizeof(h) * c->myrow, &h, sizeof(h), cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(dh + sizeof(h) * c->myrow, h, sizeof(h), cudaMemcpyHostToDevice));
     NK(c, ncclAllGather(dh + sizeof(h) * c->myrow, dh, sizeof(h), ncclChar, c->col_comm, c->s_la));
     CK(c, cudaStreamSynchronize(c->s_la));
-    std::vector<cudaIpcMemHandle_t> hs(P);
+    std::vector<cudaIpcMemHandle_t> hs(3 * (size_t)P);
     CK(c, cudaMemcpy(hs.data(), dh, sizeof(h) * P, cudaMemcpyDeviceToHost));
     cudaFree(dh);
     c->xpeer.assign(P, nullptr);
+    c->apeer.assign(P, nullptr);
+    c->fpeer.assign(P, nullptr);
+    c->rsp.P = P;
+    c->rsp.myrow = c->myrow;
+    c->rsp.my_flag = c->rsflag;
+    for (int p = 0; p < P; ++p) {
+        if (p == c->myrow) {
+            c->rsp.A[p] = c->A;
+            c->rsp.flag[p] = c->rsflag;
+            continue;
+        }
+        CK(c, cudaIpcOpenMemHandle(&c->apeer[p], hs[3 * p + 1], cudaIpcMemLazyEnablePeerAccess));
+        CK(c, cudaIpcOpenMemHandle(&c->fpeer[p], hs[3 * p + 2], cudaIpcMemLazyEnablePeerAccess));
+        c->rsp.A[p] = static_cast<const double *>(c->apeer[p]);
+        c->rsp.flag[p] = static_cast<unsigned long long *>(c->fpeer[p]);
+    }
     c->xch.P = P;
     c->xch.myrow = c->myrow;
     c->xch.recd = recd;
     for (int p = 0; p < P; ++p) {
         void *base = c->xbuf;
         if (p != c->myrow) {
-            CK(c, cudaIpcOpenMemHandle(&c->xpeer[p], hs[p], cudaIpcMemLazyEnablePeerAccess));
+            CK(c, cudaIpcOpenMemHandle(&c->xpeer[p], hs[3 * p], cudaIpcMemLazyEnablePeerAccess));
             base = c->xpeer[p];
         }
         c->xch.rec[p] = static_cast<double *>(base);
@@ -497,6 +587,48 @@ hpl_status setup_exchange(hpl_ctx *c)
     }
     c->xch.my_rec = c->xch.rec[c->myrow];
     c->xch.my_flag = c->xch.flag[c->myrow];
+    return HPL_OK;
+}
+
+// Q > 1: panel buffers + LBCAST flags shared inside each process row (CUDA IPC
+// over NVLink); handles travel over the row communicator.  Flags are
+// monotonic across factorizations: panel j of a factorization is
+// lb_base + j + 1, lb_base advancing past the previous factorization's values.
+hpl_status setup_lbcast(hpl_ctx *c)
+{
+    const int Q = c->Q, NBUF = hpl_ctx::NBUF;
+    if (Q > 32) return HPL_ERR_ARG;
+    const size_t fbytes = sizeof(unsigned long long) * 64;
+    CK(c, cudaMalloc(&c->lbflag, fbytes));
+    CK(c, cudaMemset(c->lbflag, 0, fbytes));
+    std::vector<cudaIpcMemHandle_t> h(NBUF + 1);
+    for (int b = 0; b < NBUF; ++b) CK(c, cudaIpcGetMemHandle(&h[b], c->panel[b]));
+    CK(c, cudaIpcGetMemHandle(&h[NBUF], c->lbflag));
+    const size_t hb = sizeof(cudaIpcMemHandle_t) * (NBUF + 1);
+    char *dh = nullptr;
+    CK(c, cudaMalloc(&dh, hb * Q));
+    CK(c, cudaMemcpy(dh + hb * c->mycol, h.data(), hb, cudaMemcpyHostToDevice));
+    NK(c, ncclAllGather(dh + hb * c->mycol, dh, hb, ncclChar, c->row_comm, c->s_la));
+    CK(c, cudaStreamSynchronize(c->s_la));
+    std::vector<cudaIpcMemHandle_t> hs((size_t)Q * (NBUF + 1));
+    CK(c, cudaMemcpy(hs.data(), dh, hb * Q, cudaMemcpyDeviceToHost));
+    cudaFree(dh);
+    c->ppanel.assign((size_t)Q * NBUF, nullptr);
+    c->pflag.assign(Q, nullptr);
+    for (int q = 0; q < Q; ++q) {
+        for (int k = 0; k <= NBUF; ++k) {
+            void *ptr = nullptr;
+            if (q == c->mycol) {
+                ptr = k < NBUF ? (void *)c->panel[k] : (void *)c->lbflag;
+            } else {
+                CK(c, cudaIpcOpenMemHandle(&ptr, hs[(size_t)q * (NBUF + 1) + k],
+                                           cudaIpcMemLazyEnablePeerAccess));
+                c->lbpeer.push_back(ptr);
+            }
+            if (k < NBUF) c->ppanel[(size_t)q * NBUF + k] = static_cast<const double *>(ptr);
+            else c->pflag[q] = static_cast<unsigned long long *>(ptr);
+        }
+    }
     return HPL_OK;
 }
 
@@ -551,6 +683,7 @@ hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t s
     NK(c, ncclCommSplit(c->world, c->mycol, c->myrow, &c->col_comm_tr, nullptr));
     hpl_status s = alloc_ctx(c);
     if (s == HPL_OK && P > 1) s = setup_exchange(c);
+    if (s == HPL_OK && Q > 1) s = setup_lbcast(c);
     if (s == HPL_OK) s = generate(c);
     return s;
 }
@@ -579,6 +712,8 @@ hpl_status hpl_factor(hpl_ctx *c)
     }
     c->dgemm_flop = 0;
     c->dgemm_launches = 0;
+    c->lb_base = c->lb_next;
+    c->lb_next += (unsigned long long)nblk + 2;
     CK(c, cudaEventRecord(c->ev_t[0], c->s_la));
     CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_t[0], 0));
     CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_t[0], 0));
@@ -940,6 +1075,8 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "split")) c->split_pct = (int)value;
     else if (!strcmp(name, "early_next")) c->early_next = value != 0;
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
+    else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
+    else if (!strcmp(name, "lb_peer")) c->lb_peer = value != 0 && c->lbflag != nullptr;
     else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }
     else if (!strcmp(name, "leaf_hide_ms")) { c->leaf_auto = true; c->leaf_hide_ms = (double)value; }
     else return HPL_ERR_ARG;

@@ -138,6 +138,37 @@ cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, c
                        int64_t ldw, int64_t j0, double *A, int64_t lda, int64_t c0, int64_t c1,
                        int NB, int P, int myrow);
 
+// P > 1 RS over peer memory: A[p] = process row p's local A (IPC-mapped; own
+// A at myrow), flag[p] = its barrier flag area (RS_SLOTS x MAX_P u64),
+// my_flag = this process's.  Process rows of one process column share lda.
+constexpr int RS_SLOTS = 8;
+struct RsPeers {
+    const double *A[MAX_P];
+    unsigned long long *flag[MAX_P];
+    unsigned long long *my_flag;
+    int P, myrow;
+};
+// Flag barrier over the process column at `slot` (monotonic value): one
+// one-warp kernel; every later kernel on st sees the peers' earlier writes.
+cudaError_t rs_barrier(cudaStream_t st, const RsPeers &pr, int slot, unsigned long long value);
+// Phase 1 of the peer-memory RS for local columns [c0, c1): U[k] = global row
+// src[k] read from its owner; W[s - j0] = original block row s (from the
+// owner of block row j0) for every displaced pair (d, s) whose d this process owns.
+cudaError_t rs_gather_peer(cudaStream_t st, int64_t jb, const int64_t *src, const int64_t *disp,
+                           const int *ndisp, const RsPeers &pr, int64_t lda, int64_t c0,
+                           int64_t c1, double *U, int64_t ldu, double *W, int64_t ldw, int64_t j0,
+                           int NB);
+
+// One flag step over peer memory (LBCAST): publish sv to each sig[i] (i <
+// nsig), then wait until every *wt[i] >= wv (i < nwait).  One one-warp kernel.
+struct FlagOp {
+    unsigned long long *sig[32];
+    const unsigned long long *wt[32];
+    int nsig, nwait;
+    unsigned long long sv, wv;
+};
+cudaError_t flag_op(cudaStream_t st, const FlagOp &op);
+
 // ---------------------------------------------------------------- solve / residual
 // Single-matrix back solve (y = column N of U's rows): hplk_back_solve.
 cudaError_t back_solve(cudaStream_t st, int64_t N, int NB, const double *U, int64_t ldu,

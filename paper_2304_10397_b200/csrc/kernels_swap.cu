@@ -159,6 +159,112 @@ rs_scatter_kernel(const int64_t *__restrict__ disp, const int *__restrict__ ndis
     }
 }
 
+// ---- P > 1 RS over peer memory (CUDA IPC over NVLink), no collective library.
+// Every process of the column maps every peer's local A.  Phase 1 (after a
+// flag barrier: every peer has finished updating these columns for
+// iteration j): gather U[k] = row src[k] from its owner's A, and — for the
+// displaced rows this process owns — the original block row they receive,
+// from the owner of block row j, into W.  Phase 2 (after a second barrier:
+// every peer has finished reading) is rs_scatter from W.
+__device__ __forceinline__ unsigned long long rs_ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void rs_st_release_sys(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// lane p < P: announce arrival at `slot` to peer p, then wait for peer p's arrival.
+__global__ void rs_barrier_kernel(RsPeers pr, int slot, unsigned long long value)
+{
+    const int p = threadIdx.x;
+    if (p >= pr.P) return;
+    __threadfence_system();
+    rs_st_release_sys(pr.flag[p] + (size_t)slot * MAX_P + pr.myrow, value);
+    while (rs_ld_acquire_sys(pr.my_flag + (size_t)slot * MAX_P + p) < value) __nanosleep(64);
+    __threadfence_system();
+}
+
+// Generic flag step (LBCAST over peer memory): lanes < nsig publish sv to
+// sig[lane] (after a system fence: this stream's earlier writes are visible
+// first); lanes < nwait spin until *wt[lane] >= wv.
+__global__ void flag_kernel(FlagOp op)
+{
+    const int l = threadIdx.x;
+    if (l < op.nsig) {
+        __threadfence_system();
+        rs_st_release_sys(op.sig[l], op.sv);
+    }
+    if (l < op.nwait)
+        while (rs_ld_acquire_sys(op.wt[l]) < op.wv) __nanosleep(128);
+    __threadfence_system();
+}
+
+constexpr int RG_UNROLL = 4;
+
+__global__ void __launch_bounds__(LS_WARPS * 32)
+rs_gather_peer_kernel(int jb, const int64_t *__restrict__ src, const int64_t *__restrict__ disp,
+                      const int *__restrict__ ndisp, RsPeers pr, long long lda, long long c0,
+                      long long c1, double *__restrict__ U, long long ldu,
+                      double *__restrict__ W, long long ldw, long long j0, int NB, int vec)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long col = c0 + (long long)blockIdx.x * LS_COLS + 2 * lane;
+    const bool has0 = col < c1, has1 = col + 1 < c1;
+    const int P = pr.P;
+    // row k of U (k < jb) or, for k >= jb, the displaced row slot k - jb
+    const int nd = *ndisp;
+    const int bowner = (int)((j0 / NB) % P);
+    const int total = jb + nd;
+    for (int k0 = warp * RG_UNROLL; k0 < total; k0 += LS_WARPS * RG_UNROLL) {
+        const double *sp[RG_UNROLL];
+        double *dp[RG_UNROLL];
+#pragma unroll
+        for (int u = 0; u < RG_UNROLL; ++u) {
+            const int k = k0 + u;
+            sp[u] = nullptr;
+            dp[u] = nullptr;
+            if (k < jb) {
+                const long long g = src[k];
+                sp[u] = pr.A[(int)((g / NB) % P)] + g2l_row(g, NB, P) * lda + col;
+                dp[u] = U + (long long)k * ldu + (col - c0);
+            } else if (k < total) {
+                const long long d = disp[2 * (k - jb)], s = disp[2 * (k - jb) + 1];
+                if (owns_row(d, NB, P, pr.myrow)) {
+                    sp[u] = pr.A[bowner] + g2l_row(s, NB, P) * lda + col;
+                    dp[u] = W + (s - j0) * ldw + (col - c0);
+                }
+            }
+        }
+        if (vec && has1) {
+            double2 v[RG_UNROLL];
+#pragma unroll
+            for (int u = 0; u < RG_UNROLL; ++u)
+                if (sp[u]) v[u] = __ldcg(reinterpret_cast<const double2 *>(sp[u]));
+#pragma unroll
+            for (int u = 0; u < RG_UNROLL; ++u)
+                if (sp[u]) *reinterpret_cast<double2 *>(dp[u]) = v[u];
+        } else {
+            double v0[RG_UNROLL], v1[RG_UNROLL];
+#pragma unroll
+            for (int u = 0; u < RG_UNROLL; ++u)
+                if (sp[u]) {
+                    v0[u] = has0 ? __ldcg(sp[u]) : 0.0;
+                    v1[u] = has1 ? __ldcg(sp[u] + 1) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < RG_UNROLL; ++u)
+                if (sp[u]) {
+                    if (has0) dp[u][0] = v0[u];
+                    if (has1) dp[u][1] = v1[u];
+                }
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t rs_pack(cudaStream_t st, int64_t jb, const int64_t *src, const double *A, int64_t lda,
@@ -178,6 +284,39 @@ cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, c
     if (c1 <= c0) return cudaSuccess;
     rs_scatter_kernel<<<(unsigned)cdiv(c1 - c0, LS_COLS), LS_WARPS * 32, 0, st>>>(
         disp, ndisp, W, ldw, j0, A, lda, c0, c1, NB, P, myrow);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t rs_barrier(cudaStream_t st, const RsPeers &pr, int slot, unsigned long long value)
+{
+    if (pr.P < 1 || pr.P > MAX_P || slot < 0 || slot >= RS_SLOTS) return cudaErrorInvalidValue;
+    rs_barrier_kernel<<<1, 32, 0, st>>>(pr, slot, value);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t rs_gather_peer(cudaStream_t st, int64_t jb, const int64_t *src, const int64_t *disp,
+                           const int *ndisp, const RsPeers &pr, int64_t lda, int64_t c0,
+                           int64_t c1, double *U, int64_t ldu, double *W, int64_t ldw, int64_t j0,
+                           int NB)
+{
+    if (jb <= 0 || c1 <= c0) return cudaSuccess;
+    bool vec = (lda & 1) == 0 && (c0 & 1) == 0 && (ldu & 1) == 0 && (ldw & 1) == 0 &&
+               (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&
+               (reinterpret_cast<uintptr_t>(W) & 15) == 0;
+    for (int p = 0; p < pr.P; ++p) vec = vec && (reinterpret_cast<uintptr_t>(pr.A[p]) & 15) == 0;
+    rs_gather_peer_kernel<<<(unsigned)cdiv(c1 - c0, LS_COLS), LS_WARPS * 32, 0, st>>>(
+        (int)jb, src, disp, ndisp, pr, lda, c0, c1, U, ldu, W, ldw, j0, NB, vec ? 1 : 0);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t flag_op(cudaStream_t st, const FlagOp &op)
+{
+    if (op.nsig < 0 || op.nsig > 32 || op.nwait < 0 || op.nwait > 32) return cudaErrorInvalidValue;
+    if (op.nsig == 0 && op.nwait == 0) return cudaSuccess;
+    flag_kernel<<<1, 32, 0, st>>>(op);
     count_launch();
     return cudaGetLastError();
 }

@@ -112,3 +112,26 @@ def test_2x1_warp_leaf(opts):
         pytest.skip("needs 2 GPUs")
     out = _run(2, 3000, 128, 2, 1, opts)
     assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
+
+
+
+@pytest.mark.parametrize("P,Q,split", [(2, 1, 0), (2, 1, 30), (1, 2, 0), (2, 2, 0)])
+def test_peer_exchange_vs_nccl(P, Q, split):
+    """The RS and LBCAST over NVLink peer memory (defaults: rs_peer, lb_peer)
+    and their NCCL versions (all-reduce + broadcast RS, broadcast LBCAST) both
+    give the oracle's pivots and x, with and without the split update."""
+    if _ngpu() < P * Q:
+        pytest.skip(f"needs {P * Q} GPUs")
+    for v in (1, 0):
+        out = _run(P * Q, 3000, 128, P, Q,
+                   (f"--opt=rs_peer={v}", f"--opt=lb_peer={v}", f"--opt=split={split}"))
+        assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16, (v, out)
+
+
+def test_peer_exchange_two_factorizations():
+    """Flags are monotonic across factorizations of one context (hpl_regenerate
+    then a second hpl_factor): the second solve still matches the oracle."""
+    if _ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    out = _run(4, 2048, 64, 2, 2, ("--repeat", "2"))
+    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16

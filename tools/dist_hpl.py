@@ -1,7 +1,7 @@
 """Multi-rank HPL through the C ABI (one process per GPU).
 
     torchrun --nproc-per-node Q --master-addr 127.0.0.1 --master-port PORT \\
-        tools/dist_hpl.py N NB P Q [seed] [--oracle] [--la 0|1]
+        tools/dist_hpl.py N NB P Q [seed] [--oracle] [--la 0|1] [--repeat K] [--opt=k=v]
 
 rank 0 creates the NCCL unique id (hpl_get_unique_id); it travels to the other
 ranks over a gloo process group; every rank then calls hpl_init_dist.  With
@@ -43,6 +43,11 @@ def main():
         k, v = kv[len("--opt="):].split("=")
         H.hpl_set_option(ctx, k, int(v))
     timeline = "--timeline" in sys.argv
+    repeat = int(sys.argv[sys.argv.index("--repeat") + 1]) if "--repeat" in sys.argv else 1
+    for _ in range(repeat - 1):      # earlier factorizations of the same context
+        H.hpl_factor(ctx)
+        H.hpl_solve(ctx, want_x=False)
+        H.hpl_regenerate(ctx)
     if timeline:
         H.hpl_set_timing(ctx, True)
         H.hpl_factor(ctx)            # warm-up pass

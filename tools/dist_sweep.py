@@ -17,6 +17,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 DEFAULTS = dict(lookahead=1, leaf_few_ctas=8, leaf_hide_ms=60, hp_trsm=1, split=0, early_next=0)
+DIST_DEFAULTS = dict(rs_peer=1, lb_peer=1)
 
 
 def main():
@@ -40,7 +41,7 @@ def main():
     H.hpl_solve(ctx, want_x=False)
     for rep in range(2):
         for sset in sets:
-            opts = dict(DEFAULTS)
+            opts = dict(DEFAULTS, **(DIST_DEFAULTS if world > 1 else {}))
             for kv in filter(None, sset.split(",")):
                 k, v = kv.split("=")
                 opts[k] = int(v)
