@@ -198,7 +198,7 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("gloo")   # rendezvous + scalars; the data path is libhpl's NCCL
+        dist.init_process_group("gloo")   # rendezvous + scalars; the data path is libhpl (NCCL + peer memory)
 
     def barrier():
         torch.cuda.synchronize()
@@ -322,9 +322,10 @@ def main():
         "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
         "config": {"workload": f"HPL N={N} NB={NB} {P}x{Q} grid", "N": N, "NB": NB,
                    "grid": f"{P}x{Q}", "parallelism": "1 GPU" if world == 1 else
-                   f"2D block-cyclic {P}x{Q}: NCCL LBCAST along process rows"
-                   + (", pivot exchange over NVLink peer memory + NCCL RS along process columns"
-                      if P > 1 else ""),
+                   f"2D block-cyclic {P}x{Q}: LBCAST as copy-engine pulls over NVLink peer memory"
+                   " along process rows"
+                   + (", pivot search and RS row exchange over NVLink peer memory along process"
+                      " columns" if P > 1 else ""),
                    "lookahead": True, "l2": "inputs (~137 GB per GPU) >> L2, no flush needed",
                    "residual_max": max(resids), "frac_of_fp64_peak": value / world / FP64_PEAK_DERIVED},
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (trailing update)",

@@ -28,12 +28,17 @@ def _port():
 
 
 def _run(nproc, N, NB, P, Q, extra=()):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "dist_hpl.py"), str(N), str(NB), str(P), str(Q), "42",
-           "--oracle", *extra]
     env = dict(os.environ, PYTHONPATH=ROOT)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    for attempt in range(3):
+        # the free port picked here can be taken before torchrun binds it: retry
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_port()),
+               os.path.join(ROOT, "tools", "dist_hpl.py"), str(N), str(NB), str(P), str(Q), "42",
+               "--oracle", *extra]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr + r.stdout:
+            break
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return json.loads(lines[-1])
