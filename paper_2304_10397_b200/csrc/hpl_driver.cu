@@ -87,6 +87,8 @@ struct hpl_ctx {
     cudaEvent_t ev_panel[NBUF] = {}, ev_rest = nullptr;
     cudaEvent_t ev_next = nullptr;   // rest(j) has updated panel j+2's columns
     cudaEvent_t ev_trsm = nullptr;   // rest(j)'s LASWP+DTRSM done: FACT(j+1) may start
+    cudaEvent_t ev_trsm0 = nullptr;  // DTRSM of the first column chunk done (trsm_pipe)
+    int trsm_pipe = 1;               // DTRSM/DGEMM column chunks of rest(j) (1 = one launch each)
     // split update: RS of one section overlaps the UPDATE of the other
     cudaStream_t s_rs = nullptr;
     cudaEvent_t ev_rsR = nullptr, ev_rsL = nullptr, ev_dgR = nullptr, ev_dgL = nullptr;
@@ -479,6 +481,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     CK(c, cudaEventCreateWithFlags(&c->ev_next, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_trsm, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_trsm0, cudaEventDisableTiming));
     for (int k = 0; k < 3; ++k) CK(c, cudaEventCreate(&c->ev_t[k]));
     return HPL_OK;
 }
@@ -520,6 +523,7 @@ void release(hpl_ctx *c)
     fact_work_free(&c->fw);
     if (c->ev_rest) cudaEventDestroy(c->ev_rest);
     if (c->ev_trsm) cudaEventDestroy(c->ev_trsm);
+    if (c->ev_trsm0) cudaEventDestroy(c->ev_trsm0);
     for (cudaEvent_t e : {c->ev_rsR, c->ev_rsL, c->ev_dgR, c->ev_dgL})
         if (e) cudaEventDestroy(e);
     if (c->s_rs) cudaStreamDestroy(c->s_rs);
@@ -802,13 +806,32 @@ hpl_status hpl_factor(hpl_ctx *c)
                 s = rs_cols(c, c->s_rs, j, b, lrest, cend, SEC_RIGHT, c->col_comm_tr, &rs);
                 if (s != HPL_OK) return s;
                 if (E) CK(c, cudaEventRecord(E[1], c->s_rs));
-                s = compute_cols(c, c->s_rs, j, b, lrest, cend, rs, E ? E[2] : nullptr, false,
-                                 c->ev_trsm, true, false);
+                // DTRSM / DGEMM pipelined over column chunks (option trsm_pipe =
+                // chunk count): the DGEMM of chunk 0 starts as soon as its DTRSM is
+                // done and hides the DTRSM of the remaining chunks
+                const int64_t n = cend - lrest;
+                int64_t w1 = n;
+                if (c->trsm_pipe > 1 && n >= 8 * 1024)
+                    w1 = std::min<int64_t>(n, round_up(cdiv(n, c->trsm_pipe), 64));
+                s = compute_cols(c, c->s_rs, j, b, lrest, lrest + w1, rs, E ? E[2] : nullptr, false,
+                                 w1 < n ? c->ev_trsm0 : c->ev_trsm, true, false);
                 if (s != HPL_OK) return s;
-                CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_trsm, 0));
-                s = compute_cols(c, c->s_tr, j, b, lrest, cend, rs, nullptr, E != nullptr, nullptr,
-                                 false, true);
+                RsOut rs1{rs.u + w1, rs.ldu};
+                if (w1 < n) {
+                    s = compute_cols(c, c->s_rs, j, b, lrest + w1, cend, rs1, nullptr, false,
+                                     c->ev_trsm, true, false);
+                    if (s != HPL_OK) return s;
+                }
+                CK(c, cudaStreamWaitEvent(c->s_tr, w1 < n ? c->ev_trsm0 : c->ev_trsm, 0));
+                s = compute_cols(c, c->s_tr, j, b, lrest, lrest + w1, rs, nullptr, E != nullptr,
+                                 nullptr, false, true);
                 if (s != HPL_OK) return s;
+                if (w1 < n) {
+                    CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_trsm, 0));
+                    s = compute_cols(c, c->s_tr, j, b, lrest + w1, cend, rs1, nullptr, E != nullptr,
+                                     nullptr, false, true);
+                    if (s != HPL_OK) return s;
+                }
                 if (E) CK(c, cudaEventRecord(E[3], c->s_tr));
                 CK(c, cudaEventRecord(c->ev_next, c->s_tr));
             } else {
@@ -1076,6 +1099,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "early_next")) c->early_next = value != 0;
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
+    else if (!strcmp(name, "trsm_pipe")) c->trsm_pipe = (int)std::max<int64_t>(1, value);
     else if (!strcmp(name, "lb_peer")) c->lb_peer = value != 0 && c->lbflag != nullptr;
     else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }
     else if (!strcmp(name, "leaf_hide_ms")) { c->leaf_auto = true; c->leaf_hide_ms = (double)value; }

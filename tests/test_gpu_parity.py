@@ -194,6 +194,22 @@ def test_split_update_single_gpu_invariance(H):
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
 
 
+def test_trsm_pipe_invariance(H):
+    """DTRSM / DGEMM pipelined over column chunks (option trsm_pipe; active
+    while the trailing width >= 8192) moves no arithmetic between columns:
+    pivots and x bitwise equal to the one-launch schedule."""
+    def run(k):
+        with H.hpl_init(10240, 256, 1, 1, 19) as ctx:
+            H.hpl_set_option(ctx, "trsm_pipe", k)
+            H.hpl_factor(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+    xa, pa, ra = run(1)
+    xb, pb, rb = run(4)
+    xc, pc, rc = run(3)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
+    assert np.array_equal(pa, pc) and np.array_equal(xa, xc) and rc < 16
+
+
 @pytest.mark.parametrize("opts", [{"leaf_warp": 148, "leaf_hide_ms": 0},
                                   {"leaf_warp": 7, "leaf_hide_ms": 0},
                                   {"leaf_ctas": 3}, {"leaf_ctas": 0}])
