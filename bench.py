@@ -52,6 +52,25 @@ def workload(a, world: int):
     return n, a.nb, P, Q
 
 
+def cublas_dgemm_tflops(torch) -> float:
+    """Library context for the DGEMM roofline: cuBLAS DGEMM 8192^3 through
+    torch.matmul(float64), best of 10 (SURVEY.md §8(d) measured-peak (ii))."""
+    a = torch.rand(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.rand(8192, 8192, dtype=torch.float64, device="cuda")
+    c = torch.matmul(a, b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = float("inf")
+    for _ in range(10):
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b, c
+    torch.cuda.empty_cache()
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
 def hpl_flops(n: int) -> float:
     return 2.0 / 3.0 * n ** 3 + 1.5 * n ** 2
 
@@ -223,6 +242,7 @@ def main():
         ctx = H.hpl_init_dist(N, NB, P, Q, a.seed, rank, world, bytes(uid.tolist()), local)
     H.hpl_set_timing(ctx, True)
     peak_meas = H.hplk_dmma_peak()
+    cublas_tf = cublas_dgemm_tflops(torch)
 
     fl = hpl_flops(N)
     resids = []
@@ -335,7 +355,8 @@ def main():
                      "launches": dg_n // max(1, a.steps),
                      "peak_source": "derived 148 SM x 128 FP64 flop/clk x 1965 MHz (MEASURED_PEAKS"
                                     ".json has no FP64 entry)",
-                     "peak_measured_dmma": peak_meas},
+                     "peak_measured_dmma": peak_meas,
+                     "cublas_dgemm_8192": cublas_tf},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
