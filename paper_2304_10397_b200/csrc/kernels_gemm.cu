@@ -394,6 +394,11 @@ using CfgC = Cfg<64, 64, 32, 32, 4, 3>;
 using CfgD = Cfg<64, 64, 32, 32, 6, 2>;
 // 64x64 tile, 4 CTAs/SM, 3 stages (more warps to cover epilogues).
 using CfgE = Cfg<64, 64, 32, 32, 3, 4>;
+// 64x64 tile, 8 consumer warps (32x16 each), 3 CTAs/SM: 6 DMMA warps per SM
+// sub-partition instead of 3 (more issue slack, 1.5x the LDS bytes per DMMA).
+using CfgF = Cfg<64, 64, 32, 16, 4, 3>;
+// 64x64 tile, 8 consumer warps (32x16), 2 CTAs/SM, 6 stages.
+using CfgG = Cfg<64, 64, 32, 16, 6, 2>;
 
 int g_default_cfg = 2;
 int g_tiles_per_cta = 1;
@@ -484,6 +489,8 @@ cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n,
     case 2: return launch_cfg<CfgC>(st, ma, mb, p, slot);
     case 3: return launch_cfg<CfgD>(st, ma, mb, p, slot);
     case 4: return launch_cfg<CfgE>(st, ma, mb, p, slot);
+    case 5: return launch_cfg<CfgF>(st, ma, mb, p, slot);
+    case 6: return launch_cfg<CfgG>(st, ma, mb, p, slot);
     default: return launch_cfg<CfgA>(st, ma, mb, p, slot);
     }
 }

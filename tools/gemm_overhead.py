@@ -5,7 +5,7 @@
     mainloop grows with k, its prologue/epilogue do not) under the tile
     configs and epilogue / persistence variants (cfg = 1000*red + 100*tpc + cfg).
 
-    python tools/gemm_overhead.py [m]"""
+    python tools/gemm_overhead.py [m] [cfg ...]"""
 import json
 import os
 import sys
@@ -14,12 +14,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2304_10397_b200 as H  # noqa: E402
 
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+cfgs = [int(c) for c in sys.argv[2:]] or [2, 1002, 202, 402, 3, 4, 0]
 peak = H.hplk_dmma_peak()
 for bps, w in ((1, 4), (1, 8), (1, 12), (3, 4), (1, 16), (2, 8), (4, 4)):
     tf = H.hplk_dmma_peak(20000, bps, w)
     print(json.dumps(dict(dmma_blocks_per_sm=bps, warps=w, warps_per_smsp=bps * w / 4,
                           tflops=round(tf, 3))), flush=True)
-for cfg in (2, 1002, 202, 402, 3, 4, 0):
+for cfg in cfgs:
     for k in (512, 2048):
         ms = min(H.hplk_dgemm_bench(m, m, k, cfg=cfg, reps=5))
         tf = 2 * m * m * k / (ms * 1e-3) / 1e12
