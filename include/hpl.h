@@ -63,7 +63,13 @@ hpl_status hpl_init(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t seed,
 /* Multi-process context (collective over nranks = P*Q processes, one per GPU).
  * rank = p + q*P; nccl_unique_id points to the 128-byte ncclUniqueId that
  * rank 0 created and every rank received out of band (e.g. through
- * torch.distributed); device is the CUDA ordinal this rank drives. */
+ * torch.distributed); device is the CUDA ordinal this rank drives.
+ * All ranks must be on one node with peer access (NVLink/NVSwitch): the
+ * context exchanges CUDA IPC handles (over NCCL) so that the P processes of a
+ * process column map each other's local matrix, pivot-exchange area and RS
+ * flags, and the Q processes of a process row map each other's panel buffers
+ * and LBCAST flags.  A failed IPC
+ * open returns HPL_ERR_CUDA. */
 hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t seed,
                          int32_t rank, int32_t nranks, const void *nccl_unique_id,
                          int32_t device, hpl_ctx **out);
@@ -120,7 +126,18 @@ int64_t hpl_get_timeline(const hpl_ctx *ctx, double *t, int64_t cap);
 int64_t hpl_get_fact_detail(const hpl_ctx *ctx, double *t, int64_t cap);
 /* Enable per-phase CUDA events (adds a little host work per iteration). */
 hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
-/* Tuning knobs: lookahead on/off (default on). */
+/* Tuning / A-B knobs (none changes the pivots or x; tested):
+ *   lookahead 0|1 (1)      look-ahead depth 1 on a high-priority stream
+ *   split <pct> (0)        split update, right-section share
+ *   rs_peer 0|1 (1)        P>1 RS over NVLink peer memory; 0 = NCCL all-reduce + broadcast
+ *   lb_peer 0|1 (1)        Q>1 LBCAST as copy-engine pulls; 0 = NCCL broadcast
+ *   hp_trsm 0|1 (1)        rest LASWP + DTRSM on the high-priority stream
+ *   trsm_pipe <k> (1)      DTRSM/DGEMM of the rest pipelined over k column chunks
+ *   nbmin <1..16> (16)     recursion base width of the panel FACT
+ *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas, leaf_rows   leaf grid policy
+ *   gemm_cfg, gemm_tpc, gemm_red   DGEMM tile config / tiles per CTA / RED epilogue
+ *   early_next 0|1 (0)     update panel j+2's columns first inside rest(j)
+ * Unknown names return HPL_ERR_ARG. */
 hpl_status hpl_set_option(hpl_ctx *ctx, const char *name, int64_t value);
 /* Number of this library's kernel launches in the last hpl_factor + hpl_solve. */
 int64_t hpl_launch_count(const hpl_ctx *ctx);
