@@ -96,6 +96,7 @@ struct hpl_ctx {
     // options
     bool lookahead = true;
     bool hp_trsm = true;             // rest RS + DTRSM on the high-priority stream
+    bool store_l = true;             // write L21 back into A (the solve needs only U and y)
     bool early_next = false;         // (option) update panel j+2's columns first inside rest(j)
     int nbmin = 16;
     bool leaf_auto = true;           // adaptive leaf grid (fact_panel)
@@ -195,7 +196,8 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
         CK(c, rm_to_cm(st, jb + mL, jb, Ablk, c->lda, c->panel[b], ldpj));
         CK(c, panel_fact(st, jb + mL, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin,
                          &c->fw, c->scratch, j0));
-        CK(c, cm_to_rm(st, jb + mL, jb, c->panel[b], ldpj, Ablk, c->lda));
+        // write back L11\U11 (U is part of the result); L21 only with store_l
+        CK(c, cm_to_rm(st, c->store_l ? jb + mL : jb, jb, c->panel[b], ldpj, Ablk, c->lda));
         return HPL_OK;
     }
     // T from the owner of block row j to the whole process column
@@ -212,7 +214,8 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
     df.seq = &c->xseq;
     CK(c, panel_fact(st, jb + mL, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin, &c->fw,
                      c->scratch, j0, &df));
-    CK(c, cm_to_rm(st, mL, jb, c->panel[b] + jb, ldpj, c->A + lrL0 * c->lda + lcp, c->lda));
+    if (c->store_l)
+        CK(c, cm_to_rm(st, mL, jb, c->panel[b] + jb, ldpj, c->A + lrL0 * c->lda + lcp, c->lda));
     if (is_prow) CK(c, cm_to_rm(st, jb, jb, c->panel[b], ldpj, c->A + lr0 * c->lda + lcp, c->lda));
     return HPL_OK;
 }
@@ -1099,6 +1102,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "early_next")) c->early_next = value != 0;
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
+    else if (!strcmp(name, "store_l")) c->store_l = value != 0;
     else if (!strcmp(name, "trsm_pipe")) c->trsm_pipe = (int)std::max<int64_t>(1, value);
     else if (!strcmp(name, "lb_peer")) c->lb_peer = value != 0 && c->lbflag != nullptr;
     else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }

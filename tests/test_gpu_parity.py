@@ -194,6 +194,22 @@ def test_split_update_single_gpu_invariance(H):
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
 
 
+def test_store_l_invariance(H):
+    """Skipping the L21 write-back (option store_l=0: the solve needs only U
+    and y = L^-1 P b) leaves the pivots, x and the upper triangle bitwise
+    unchanged."""
+    def run(v):
+        with H.hpl_init(3000, 128, 1, 1, 23) as ctx:
+            H.hpl_set_option(ctx, "store_l", v)
+            H.hpl_factor(ctx)
+            LU = H.hpl_get_local(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), np.triu(LU[:, :3000]), H.hpl_residual(ctx)
+    xa, pa, ua, ra = run(1)
+    xb, pb, ub, rb = run(0)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and np.array_equal(ua, ub)
+    assert rb < 16
+
+
 def test_trsm_pipe_invariance(H):
     """DTRSM / DGEMM pipelined over column chunks (option trsm_pipe; active
     while the trailing width >= 8192) moves no arithmetic between columns:
