@@ -137,7 +137,9 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas, leaf_rows   leaf grid policy
  *   gemm_cfg, gemm_tpc, gemm_red   DGEMM tile config / tiles per CTA / RED epilogue
  *   early_next 0|1 (0)     update panel j+2's columns first inside rest(j)
- * Unknown names return HPL_ERR_ARG. */
+ * Unknown names return HPL_ERR_ARG.  On a multi-process context every rank
+ * must set the same options before the same hpl_factor (the schedule decides
+ * which collectives and peer-memory barriers are issued). */
 hpl_status hpl_set_option(hpl_ctx *ctx, const char *name, int64_t value);
 /* Number of this library's kernel launches in the last hpl_factor + hpl_solve. */
 int64_t hpl_launch_count(const hpl_ctx *ctx);

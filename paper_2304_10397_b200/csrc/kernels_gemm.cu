@@ -147,11 +147,18 @@ struct alignas(64) ParamPad {
     unsigned char b[64 * (SLOT + 1)];
 };
 
-template <class C, int SLOT, bool RED>
+// EPI: 0 = C -= acc through registers (C prefetched to L2), 1 = red.global.add
+// of -acc per element, 2 = -acc staged in shared memory (the drained stage
+// ring) and added to C by one TMA reduce-add of the whole tile
+// (cp.reduce.async.bulk.tensor .add: the L2 performs C + (-acc), one rounding,
+// bitwise equal to C - acc).  EPI 2 needs one tile per CTA.
+template <class C, int SLOT, int EPI>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
 dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
-                 const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB)
+                 const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC)
 {
+    constexpr bool RED = EPI == 1;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -227,7 +234,7 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     const int row_base = m0 + wm * C::WM;   // first row of this warp's tile
     const int col_base = n0 + wn * C::WN;
 
-    if (p.prefetch_c && p.mode == GEMM_UPDATE) {
+    if (EPI != 2 && p.prefetch_c && p.mode == GEMM_UPDATE) {
         // Pull this warp's C tile toward L2 while the mainloop runs: each lane
         // touches the 128-byte lines of its own rows.
         for (int r = lane; r < C::WM; r += 32) {
@@ -292,6 +299,37 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     }
 
     // ================= epilogue: C -= acc  (or C = acc) =================
+    if constexpr (EPI == 2) {
+        // every consumer has finished reading the ring (the producer issued
+        // exactly this tile's stages, all consumed): reuse it for the tile
+        asm volatile("bar.sync 1, %0;" ::"n"(C::NCW * 32) : "memory");
+        double *stile = reinterpret_cast<double *>(smem);
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = wm * C::WM + 16 * i + 2 * g + h;
+#pragma unroll
+                for (int j = 0; j < C::NJ; ++j) {
+                    const int cc = wn * C::WN + 16 * j + 4 * t;
+                    double2 *q = reinterpret_cast<double2 *>(stile + r * C::BN + cc);
+                    q[0] = make_double2(-acc[i][j][0][2 * h], -acc[i][j][1][2 * h]);
+                    q[1] = make_double2(-acc[i][j][0][2 * h + 1], -acc[i][j][1][2 * h + 1]);
+                }
+            }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(C::NCW * 32) : "memory");
+        if (warp == 0 && lane == 0) {
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
+                " [%0, {%1, %2}], [%3];" ::"l"(reinterpret_cast<uint64_t>(&tmC)),
+                "r"(n0), "r"(m0), "r"(smem_base)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        continue;
+    }
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
 #pragma unroll
@@ -384,6 +422,23 @@ cudaError_t make_map(CUtensorMap *map, const double *base, int64_t xext, int64_t
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// C (row-major, ld doubles) for the TMA reduce-add epilogue: box = one tile,
+// no swizzle (the staged tile is dense row-major in shared memory).
+cudaError_t make_map_c(CUtensorMap *map, const double *base, int64_t ncols, int64_t nrows,
+                       int64_t ld, int box_cols, int box_rows)
+{
+    EncodeFn enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    cuuint64_t gdim[2] = {(cuuint64_t)ncols, (cuuint64_t)nrows};
+    cuuint64_t gstr[1] = {(cuuint64_t)(ld * 8)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), gdim,
+                     gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // 128x64 tile, 4 consumer warps (64x32 each), 2 CTAs/SM, 4 stages.
 using CfgA = Cfg<128, 64, 64, 32, 4, 2>;
 // 128x128 tile, 8 consumer warps (64x32 each), 1 CTA/SM, 6 stages.
@@ -404,21 +459,22 @@ int g_default_cfg = 2;
 int g_tiles_per_cta = 1;
 int g_red_epi = 0;
 
-// The RED epilogue is a separate instantiation (default config only): a
-// runtime branch in the epilogue made the default kernel spill.
-template <class C, int SLOT, bool RED = false>
+// The RED and TMA-reduce epilogues are separate instantiations (default
+// config only): a runtime branch in the epilogue made the default kernel spill.
+template <class C, int SLOT, int EPI = 0>
 cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
-                        const GemmParams &p)
+                        const GemmParams &p, const CUtensorMap *mc = nullptr)
 {
     static bool attr_set = false;
     if (!attr_set) {
-        HPL_CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT, RED>,
+        HPL_CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT, EPI>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
     const long long grid = cdiv(p.ntiles, p.tiles_per_cta);
     ParamPad<SLOT> pad{};
-    dgemm_tma_kernel<C, SLOT, RED><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
+    const CUtensorMap &mcr = mc ? *mc : ma;   // unused unless EPI == 2
+    dgemm_tma_kernel<C, SLOT, EPI><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb, mcr);
     count_launch();
     return cudaGetLastError();
 }
@@ -434,8 +490,20 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
     // per CTA so concurrent FACT kernels find free SM slots quickly)
     p.tiles_per_cta = p.ntiles >= 16 * 148 * C::MINB ? g_tiles_per_cta : 1;
     if constexpr (std::is_same_v<C, CfgC>) {
-        if (p.red_epi && p.mode == GEMM_UPDATE && slot == 0)
-            return launch_slot<C, 0, true>(st, ma, mb, p);
+        if (p.red_epi == 2 && p.mode == GEMM_UPDATE && p.C2 == nullptr &&
+            (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.ldc & 1) == 0) {
+            // TMA reduce-add epilogue: one tile per CTA, a C tensor map (box = tile)
+            CUtensorMap mc;
+            HPL_CUDA_TRY(make_map_c(&mc, p.C, p.n, p.m, p.ldc, C::BN, C::BM));
+            p.tiles_per_cta = 1;
+            switch (slot) {
+            case 1: return launch_slot<C, 1, 2>(st, ma, mb, p, &mc);
+            case 2: return launch_slot<C, 2, 2>(st, ma, mb, p, &mc);
+            default: return launch_slot<C, 0, 2>(st, ma, mb, p, &mc);
+            }
+        }
+        if (p.red_epi == 1 && p.mode == GEMM_UPDATE && slot == 0)
+            return launch_slot<C, 0, 1>(st, ma, mb, p);
     }
     switch (slot) {
     case 1: return launch_slot<C, 1>(st, ma, mb, p);

@@ -210,6 +210,24 @@ def test_store_l_invariance(H):
     assert rb < 16
 
 
+@pytest.mark.parametrize("epi", [1, 2])
+def test_dgemm_epilogue_variants_bitwise(H, epi):
+    """The trailing DGEMM's RED (epi 1) and TMA reduce-add (epi 2) epilogues
+    compute C + (-acc) at the L2 — one rounding, bitwise C - acc — so a whole
+    solve gives the default epilogue's pivots and x bit for bit."""
+    def run(v):
+        with H.hpl_init(3000, 128, 1, 1, 29) as ctx:
+            H.hpl_set_option(ctx, "gemm_red", v)
+            try:
+                H.hpl_factor(ctx)
+                return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+            finally:
+                H.hpl_set_option(ctx, "gemm_red", 0)   # process-wide knob
+    xa, pa, _ = run(0)
+    xb, pb, rb = run(epi)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
+
+
 def test_trsm_pipe_invariance(H):
     """DTRSM / DGEMM pipelined over column chunks (option trsm_pipe; active
     while the trailing width >= 8192) moves no arithmetic between columns:
