@@ -1103,6 +1103,10 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
     else if (!strcmp(name, "store_l")) c->store_l = value != 0;
+    else if (!strcmp(name, "leaf_variant")) {   // process-wide (like the gemm_* knobs)
+        if (value < 0 || value > 2) return HPL_ERR_ARG;
+        fact_set_leaf_variant((int)value);
+    }
     else if (!strcmp(name, "trsm_pipe")) c->trsm_pipe = (int)std::max<int64_t>(1, value);
     else if (!strcmp(name, "lb_peer")) c->lb_peer = value != 0 && c->lbflag != nullptr;
     else if (!strcmp(name, "leaf_few_ctas")) { c->leaf_auto = true; c->leaf_few_ctas = (int)value; }

@@ -101,6 +101,11 @@ void fact_set_leaf_ctas(int max_ctas, int rows_per_cta);
 // > 0: leaves run as one-warp CTAs (at most this many) that fit next to the
 // trailing DGEMM's CTAs; 0: the multi-warp leaf with fact_set_leaf_ctas' grid
 void fact_set_leaf_warp_ctas(int ctas);
+// Leaf variant of the P = 1 panel FACT: 0 right-looking
+// (default), 1 left-looking, 2 Crout — bitwise-equal results.  P > 1 panels
+// always use the right-looking distributed leaf.
+void fact_set_leaf_variant(int v);
+int fact_get_leaf_variant();
 // Pivot winner among n candidates (max |v|, ties -> smallest row), as the FACT reduces.
 cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,
                        int64_t *winner);

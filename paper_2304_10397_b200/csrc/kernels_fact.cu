@@ -212,6 +212,169 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
     }
 }
 
+// Left-looking and Crout leaves (rocHPL's FACT variants;
+// SURVEY §8(f) NEXT 3).  Same grid, same one barrier per column and the same
+// pivot rule as leaf_fact_kernel; only the data flow differs:
+//  - the column kk is brought up to date only when it is reached:
+//    v_i = a_i,kk - sum_{c<kk} l_i,c u_c,kk (FMAs in ascending c), fused with
+//    the scaling of column kk-1 for the CTA's own rows;
+//  - the U rows of the leaf are formed in shared memory by every CTA from the
+//    broadcast pivot rows: u_kk,cc = p_cc - sum_{c<kk} p_c u_c,cc;
+//  - LEFT writes u_c,kk into the rows above when column kk is reached
+//    (column-by-column triangular solve), CROUT writes the whole U row kk at
+//    its pivot step.
+// Each result goes through the same FMA sequence with the same operands as
+// the right-looking leaf's in-place updates, so all three are bitwise equal
+// (tested), and differ only in memory traffic and timing.
+template <int NT, bool CROUT>
+__global__ void __launch_bounds__(NT, 1)
+leaf_fact_ll_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, double *cand,
+                    unsigned *bar, unsigned long long *info, long long goff)
+{
+    const unsigned G = gridDim.x;
+    const int nrows = m - k0;
+    const int chunk = (nrows + (int)G - 1) / (int)G;
+    const int rbeg = k0 + (int)blockIdx.x * chunk;
+    const int rend = min(m, rbeg + chunk);
+    __shared__ double s_v[NT / 32];
+    __shared__ long long s_r[NT / 32];
+    __shared__ int s_c[NT / 32];
+    __shared__ double s_prow[LEAF_MAX], s_rowk[LEAF_MAX];
+    __shared__ double s_U[LEAF_MAX][LEAF_MAX];
+    __shared__ long long s_p;
+    __shared__ double s_piv;
+
+    double bv = -1.0;
+    long long br = LLONG_MAX;
+    for (int i = max(rbeg, k0) + threadIdx.x; i < rend; i += NT) {
+        const double v = fabs(P[(int64_t)k0 * ldp + i]);
+        if (better(v, i, bv, br)) { bv = v; br = i; }
+    }
+    for (int kk = 0; kk < w; ++kk) {
+        const int kc = k0 + kk;
+        double *rec = cand + (size_t)(kk & 1) * (MAX_CTAS + 1) * REC;
+        // ---- LEFT: the rows above reach column kk (u_c,kk, c < kk, from s_U)
+        if (!CROUT)
+            for (int c = threadIdx.x; c < kk; c += NT)
+                if (k0 + c >= rbeg && k0 + c < rend)
+                    P[(int64_t)kc * ldp + k0 + c] = s_U[c][kk];
+        // ---- 1. candidate record (|v|, row, the row's current leaf values)
+        warp_argmax(bv, br);
+        if ((threadIdx.x & 31) == 0) { s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            bv = threadIdx.x < NT / 32 ? s_v[threadIdx.x] : -1.0;
+            br = threadIdx.x < NT / 32 ? s_r[threadIdx.x] : LLONG_MAX;
+            warp_argmax(bv, br);
+            double *myrec = rec + (size_t)blockIdx.x * REC;
+            if (threadIdx.x == 0) {
+                myrec[0] = bv;
+                myrec[1] = __longlong_as_double(br);
+            }
+            if (br != LLONG_MAX && threadIdx.x < w)
+                myrec[2 + threadIdx.x] = P[(int64_t)(k0 + threadIdx.x) * ldp + br];
+            if (kc >= rbeg && kc < rend && threadIdx.x < w)
+                rec[(size_t)G * REC + 2 + threadIdx.x] = P[(int64_t)(k0 + threadIdx.x) * ldp + kc];
+        }
+        __threadfence();
+        grid_barrier(bar, G);
+
+        // ---- 2. every CTA reduces all candidates (deterministic)
+        bv = -1.0;
+        br = LLONG_MAX;
+        int bc = -1;
+        for (int c = threadIdx.x; c < (int)G; c += NT) {
+            const double v = __ldcg(rec + (size_t)c * REC);
+            const long long r = __double_as_longlong(__ldcg(rec + (size_t)c * REC + 1));
+            if (r != LLONG_MAX && better(v, r, bv, br)) { bv = v; br = r; bc = c; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_v[threadIdx.x >> 5] = bv; s_r[threadIdx.x >> 5] = br; s_c[threadIdx.x >> 5] = bc;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const bool ok = threadIdx.x < NT / 32;
+            bv = ok ? s_v[threadIdx.x] : -1.0;
+            br = ok ? s_r[threadIdx.x] : LLONG_MAX;
+            bc = ok ? s_c[threadIdx.x] : -1;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+            }
+            if (threadIdx.x == 0) {
+                s_p = br;
+                s_piv = __ldcg(rec + (size_t)bc * REC + 2 + kk);
+            }
+            if (threadIdx.x < w) {
+                s_prow[threadIdx.x] = __ldcg(rec + (size_t)bc * REC + 2 + threadIdx.x);
+                s_rowk[threadIdx.x] = __ldcg(rec + (size_t)G * REC + 2 + threadIdx.x);
+            }
+        }
+        __syncthreads();
+        // ---- 3. U row kk: u_kk,cc = p_cc - sum_{c<kk} l_p,c u_c,cc (every CTA)
+        if (threadIdx.x < w) {
+            const int cc = threadIdx.x;
+            double u = s_prow[cc];
+            if (cc > kk)
+                for (int c = 0; c < kk; ++c) u = fma(-s_prow[c], s_U[c][cc], u);
+            s_U[kk][cc] = u;
+        }
+        __syncthreads();
+        const long long p = s_p;
+        const double piv = s_piv;
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            ipiv[kc] = p;
+            if (piv == 0.0) atomicMin(info, (unsigned long long)(goff + kc));
+        }
+        // ---- 4. swap rows kc and p inside the leaf columns (owners); CROUT
+        // stores the finished U row kk into row kc right away
+        if (kc >= rbeg && kc < rend && threadIdx.x < w)
+            P[(int64_t)(k0 + threadIdx.x) * ldp + kc] =
+                (CROUT && threadIdx.x > kk) ? s_U[kk][threadIdx.x] : s_prow[threadIdx.x];
+        if (p != kc && p >= rbeg && p < rend && threadIdx.x < w)
+            P[(int64_t)(k0 + threadIdx.x) * ldp + p] = s_rowk[threadIdx.x];
+        __syncthreads();
+        // ---- 5. own rows > kc: scale column kk; bring column kk+1 up to date
+        // (one load per needed column, all before the stores); next candidate
+        bv = -1.0;
+        br = LLONG_MAX;
+        const bool more = kk + 1 < w;
+        for (int i = max(rbeg, kc + 1) + threadIdx.x; i < rend; i += NT) {
+            double x[LEAF_MAX];
+#pragma unroll
+            for (int c = 0; c < LEAF_MAX; ++c)
+                x[c] = (c <= kk + 1 && c < w) ? P[(int64_t)(k0 + c) * ldp + i] : 0.0;
+            double l = 0.0;
+#pragma unroll
+            for (int c = 0; c < LEAF_MAX; ++c)
+                if (c == kk) l = x[c] / piv;
+            P[(int64_t)kc * ldp + i] = l;
+            if (more) {
+                double v = 0.0;
+#pragma unroll
+                for (int c = 0; c < LEAF_MAX; ++c)
+                    if (c == kk + 1) v = x[c];
+#pragma unroll
+                for (int c = 0; c < LEAF_MAX; ++c)
+                    if (c <= kk) v = fma(-(c == kk ? l : x[c]), s_U[c][kk + 1], v);
+                P[(int64_t)(kc + 1) * ldp + i] = v;
+                if (better(fabs(v), i, bv, br)) { bv = fabs(v); br = i; }
+            }
+        }
+    }
+    // LEFT: nothing is pending (column w-1's U entries were written at step w-1)
+}
+
 // Apply the leaf's swaps (ipiv[k0..k0+w), panel-relative) to the panel columns
 // outside the leaf, dlaswp semantics.  Thread 0 turns the <= 16 sequential
 // swaps into "row r receives the old content of row s" moves (as pivot_plan
@@ -468,6 +631,7 @@ int g_num_sms = 0;
 int g_leaf_max_ctas = 0;        // 0 = all SMs
 int g_leaf_rows_per_cta = 512;
 int g_leaf_warp_ctas = 0;       // > 0: one-warp CTAs (co-resident with the DGEMM), at most this many
+int g_leaf_variant = 0;         // 0 right-looking, 1 left-looking, 2 Crout (leaf_fact_ll_kernel)
 constexpr int WARP_LEAF_MIN_ROWS = 128;
 
 // grid of the next leaf launch: {CTAs, threads per CTA}
@@ -502,6 +666,12 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int 
     void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->bar, &info, &goff};
     const void *fn = NT == 32 ? (const void *)leaf_fact_kernel<32>
                               : (const void *)leaf_fact_kernel<FACT_THREADS>;
+    if (g_leaf_variant == 1)
+        fn = NT == 32 ? (const void *)leaf_fact_ll_kernel<32, false>
+                      : (const void *)leaf_fact_ll_kernel<FACT_THREADS, false>;
+    else if (g_leaf_variant == 2)
+        fn = NT == 32 ? (const void *)leaf_fact_ll_kernel<32, true>
+                      : (const void *)leaf_fact_ll_kernel<FACT_THREADS, true>;
     HPL_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), args, 0, st));
     count_launch();
     if (w < 0) return cudaErrorInvalidValue;
@@ -600,6 +770,8 @@ cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64
 }
 
 void fact_set_leaf_warp_ctas(int ctas) { g_leaf_warp_ctas = ctas; }
+void fact_set_leaf_variant(int v) { g_leaf_variant = (v >= 0 && v <= 2) ? v : 0; }
+int fact_get_leaf_variant() { return g_leaf_variant; }
 
 void fact_set_leaf_ctas(int max_ctas, int rows_per_cta)
 {

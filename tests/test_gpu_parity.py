@@ -100,6 +100,42 @@ def test_panel_fact_vs_oracle(H, m, nb, nbmin):
     assert np.max(np.abs(LU - LUo)) <= 1e-12
 
 
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("m,nb,nbmin", [(5000, 128, 16), (777, 64, 16), (3000, 256, 8),
+                                        (40, 40, 16), (1200, 96, 4)])
+def test_panel_fact_leaf_variants(H, variant, m, nb, nbmin):
+    """Left-looking (1) and Crout (2) leaves against the
+    oracle, and bitwise against the right-looking leaf (same FMA sequences)."""
+    Pn = hpl_panel(m, nb, seed=3 * m + nb)
+    LU0, ip0, _ = H.hplk_panel_fact(Pn, nbmin=nbmin)
+    with H.hpl_init(64, 16, 1, 1, 1) as ctx:   # the knob is process-wide
+        H.hpl_set_option(ctx, "leaf_variant", variant)
+        try:
+            LU, ipiv, info = H.hplk_panel_fact(Pn, nbmin=nbmin)
+        finally:
+            H.hpl_set_option(ctx, "leaf_variant", 0)
+    LUo, ipo, _ = oracle.getrf(Pn)
+    assert info == -1 and np.array_equal(ipiv, ipo)
+    assert np.max(np.abs(LU - LUo)) <= 1e-12
+    assert np.array_equal(ipiv, ip0) and np.array_equal(LU, LU0)
+
+
+def test_leaf_variant_end_to_end(H):
+    """A whole solve with each leaf variant: pivots and x bitwise equal."""
+    def run(v):
+        with H.hpl_init(3000, 128, 1, 1, 31) as ctx:
+            H.hpl_set_option(ctx, "leaf_variant", v)
+            try:
+                H.hpl_factor(ctx)
+                return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+            finally:
+                H.hpl_set_option(ctx, "leaf_variant", 0)
+    x0, p0, _ = run(0)
+    for v in (1, 2):
+        x, p, r = run(v)
+        assert np.array_equal(p, p0) and np.array_equal(x, x0) and r < 16
+
+
 def test_panel_fact_special(H):
     LU, ipiv, info = H.hplk_panel_fact(np.array([[0.0], [3.0]]), nbmin=1)
     assert list(ipiv) == [1] and LU[0, 0] == 3.0 and LU[1, 0] == 0.0 and info == -1
