@@ -134,6 +134,10 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *   hp_trsm 0|1 (1)        rest LASWP + DTRSM on the high-priority stream
  *   trsm_pipe <k> (1)      DTRSM/DGEMM of the rest pipelined over k column chunks
  *   nbmin <1..16> (16)     recursion base width of the panel FACT
+ *   fact_gather <rows> (32768)  P>1: panels with at most this many global rows
+ *                          are factored whole on every GPU of the process column
+ *                          (gathered over peer memory) instead of by the
+ *                          distributed leaf; 0 = always distributed
  *   leaf_variant 0|1|2 (0) P=1 FACT leaf: right-looking / left-looking / Crout
  *                          (bitwise-equal results; process-wide)
  *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas, leaf_rows   leaf grid policy

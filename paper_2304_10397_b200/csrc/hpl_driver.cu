@@ -53,6 +53,14 @@ struct hpl_ctx {
     std::vector<void *> apeer, fpeer;
     RsPeers rsp{};
     unsigned long long rs_seq[3] = {0, 0, 0};
+    // P > 1 gathered panel FACT for small panels (option fact_gather = global
+    // rows threshold, 0 = off): the process column's packed panels, mapped
+    std::vector<void *> cpeer;
+    const double *colpanel[MAX_P][3] = {};
+    double *Cp = nullptr;            // combined panel, cp_max_rows x NB (col-major)
+    int64_t cp_max_rows = 0;
+    int64_t fact_gather_rows = 32768;
+    unsigned long long fg_seq = 0;
     // Q > 1 LBCAST over peer memory (option lb_peer, default on): the panel
     // buffers and LBCAST flags of every process column, IPC-mapped inside the
     // process row.  lbflag[o] = last panel (+1) owner o has ready;
@@ -207,6 +215,35 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
     CK(c, cudaMemcpy2DAsync(c->panel[b], ldpj * 8, c->Tbuf, jb * 8, jb * 8, jb,
                             cudaMemcpyDeviceToDevice, st));
     CK(c, rm_to_cm(st, mL, jb, c->A + lrL0 * c->lda + lcp, c->lda, c->panel[b] + jb, ldpj));
+    const int64_t rows_total = c->N - j0;   // T + every process row's L rows
+    if (c->fact_gather_rows > 0 && rows_total <= std::min(c->fact_gather_rows, c->cp_max_rows)) {
+        // Gathered FACT: barrier (every packed panel of the column is ready),
+        // build the combined panel from peer memory, barrier (every peer has
+        // read this panel), factor it here (the same arithmetic the
+        // distributed leaf performs, so the same bits), keep this process's rows.
+        const unsigned long long v = ++c->fg_seq;
+        CK(c, rs_barrier(st, c->rsp, 6, v));
+        FactPeers fp{};
+        fp.myrow = c->myrow;
+        for (int p = 0; p < c->P; ++p) {
+            const int64_t lr0p = numroc(j0, c->NB, p, c->P) + (p == prow_of(c, j) ? jb : 0);
+            const int64_t mLp = numroc(c->N, c->NB, p, c->P) - lr0p;
+            fp.panel[p] = c->colpanel[p][b];
+            fp.ld[p] = round_up(jb + mLp, 16);
+            fp.lrL0[p] = lr0p;
+        }
+        const int64_t ldc = round_up(rows_total, 16);
+        CK(c, fact_gather(st, rows_total, jb, j0, c->NB, c->P, fp, c->Cp, ldc));
+        CK(c, rs_barrier(st, c->rsp, 7, v));
+        if (c->leaf_auto) {
+            fact_set_leaf_ctas(0, 512);       // on the critical path: every SM
+            fact_set_leaf_warp_ctas(0);
+        }
+        CK(c, panel_fact(st, rows_total, jb, c->Cp, ldc, panel_ipiv(c, j, b), c->nbmin, &c->fw,
+                         c->scratch, j0));
+        CK(c, fact_extract(st, mL, jb, j0, c->NB, c->P, c->myrow, lrL0, c->Cp, ldc, c->panel[b],
+                           ldpj));
+    } else {
     DistFact df{};
     df.dp.j0 = j0; df.dp.lrL0 = lrL0; df.dp.jbp = (int)jb; df.dp.is_prow = is_prow ? 1 : 0;
     df.dp.NB = c->NB; df.dp.P = c->P; df.dp.myrow = c->myrow;
@@ -214,6 +251,7 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
     df.seq = &c->xseq;
     CK(c, panel_fact(st, jb + mL, jb, c->panel[b], ldpj, panel_ipiv(c, j, b), c->nbmin, &c->fw,
                      c->scratch, j0, &df));
+    }
     if (c->store_l)
         CK(c, cm_to_rm(st, mL, jb, c->panel[b] + jb, ldpj, c->A + lrL0 * c->lda + lcp, c->lda));
     if (is_prow) CK(c, cm_to_rm(st, jb, jb, c->panel[b], ldpj, c->A + lr0 * c->lda + lcp, c->lda));
@@ -515,6 +553,8 @@ void release(hpl_ctx *c)
     for (int k = 0; k < 3; ++k) { cudaFree(c->Ub[k]); cudaFree(c->Wb[k]); }
     for (void *pp : c->xpeer) if (pp) cudaIpcCloseMemHandle(pp);
     for (void *pp : c->apeer) if (pp) cudaIpcCloseMemHandle(pp);
+    for (void *pp : c->cpeer) if (pp) cudaIpcCloseMemHandle(pp);
+    cudaFree(c->Cp);
     for (void *pp : c->lbpeer) if (pp) cudaIpcCloseMemHandle(pp);
     cudaFree(c->lbflag);
     for (void *pp : c->fpeer) if (pp) cudaIpcCloseMemHandle(pp);
@@ -551,17 +591,20 @@ hpl_status setup_exchange(hpl_ctx *c)
     const size_t fbytes = sizeof(unsigned long long) * RS_SLOTS * MAX_P;
     CK(c, cudaMalloc(&c->rsflag, fbytes));
     CK(c, cudaMemset(c->rsflag, 0, fbytes));
-    // three handles per process row: exchange area, local A, RS flags
-    cudaIpcMemHandle_t h[3];
+    // six handles per process row: exchange area, local A, RS flags, the
+    // three packed-panel buffers (gathered FACT)
+    constexpr int NH = 6;
+    cudaIpcMemHandle_t h[NH];
     CK(c, cudaIpcGetMemHandle(&h[0], c->xbuf));
     CK(c, cudaIpcGetMemHandle(&h[1], c->A));
     CK(c, cudaIpcGetMemHandle(&h[2], c->rsflag));
+    for (int b = 0; b < 3; ++b) CK(c, cudaIpcGetMemHandle(&h[3 + b], c->panel[b]));
     char *dh = nullptr;
     CK(c, cudaMalloc(&dh, sizeof(h) * P));
     CK(c, cudaMemcpy(dh + sizeof(h) * c->myrow, h, sizeof(h), cudaMemcpyHostToDevice));
     NK(c, ncclAllGather(dh + sizeof(h) * c->myrow, dh, sizeof(h), ncclChar, c->col_comm, c->s_la));
     CK(c, cudaStreamSynchronize(c->s_la));
-    std::vector<cudaIpcMemHandle_t> hs(3 * (size_t)P);
+    std::vector<cudaIpcMemHandle_t> hs((size_t)NH * P);
     CK(c, cudaMemcpy(hs.data(), dh, sizeof(h) * P, cudaMemcpyDeviceToHost));
     cudaFree(dh);
     c->xpeer.assign(P, nullptr);
@@ -574,10 +617,17 @@ hpl_status setup_exchange(hpl_ctx *c)
         if (p == c->myrow) {
             c->rsp.A[p] = c->A;
             c->rsp.flag[p] = c->rsflag;
+            for (int b = 0; b < 3; ++b) c->colpanel[p][b] = c->panel[b];
             continue;
         }
-        CK(c, cudaIpcOpenMemHandle(&c->apeer[p], hs[3 * p + 1], cudaIpcMemLazyEnablePeerAccess));
-        CK(c, cudaIpcOpenMemHandle(&c->fpeer[p], hs[3 * p + 2], cudaIpcMemLazyEnablePeerAccess));
+        CK(c, cudaIpcOpenMemHandle(&c->apeer[p], hs[NH * p + 1], cudaIpcMemLazyEnablePeerAccess));
+        CK(c, cudaIpcOpenMemHandle(&c->fpeer[p], hs[NH * p + 2], cudaIpcMemLazyEnablePeerAccess));
+        for (int b = 0; b < 3; ++b) {
+            void *ptr = nullptr;
+            CK(c, cudaIpcOpenMemHandle(&ptr, hs[NH * p + 3 + b], cudaIpcMemLazyEnablePeerAccess));
+            c->cpeer.push_back(ptr);
+            c->colpanel[p][b] = static_cast<const double *>(ptr);
+        }
         c->rsp.A[p] = static_cast<const double *>(c->apeer[p]);
         c->rsp.flag[p] = static_cast<unsigned long long *>(c->fpeer[p]);
     }
@@ -587,7 +637,7 @@ hpl_status setup_exchange(hpl_ctx *c)
     for (int p = 0; p < P; ++p) {
         void *base = c->xbuf;
         if (p != c->myrow) {
-            CK(c, cudaIpcOpenMemHandle(&c->xpeer[p], hs[3 * p], cudaIpcMemLazyEnablePeerAccess));
+            CK(c, cudaIpcOpenMemHandle(&c->xpeer[p], hs[NH * p], cudaIpcMemLazyEnablePeerAccess));
             base = c->xpeer[p];
         }
         c->xch.rec[p] = static_cast<double *>(base);
@@ -595,6 +645,14 @@ hpl_status setup_exchange(hpl_ctx *c)
     }
     c->xch.my_rec = c->xch.rec[c->myrow];
     c->xch.my_flag = c->xch.flag[c->myrow];
+    // combined panel for the gathered FACT: up to 64 Ki global rows (2^16 x NB doubles)
+    c->cp_max_rows = std::min<int64_t>(c->N, (int64_t)1 << 16);
+    if (cudaMalloc(&c->Cp, sizeof(double) * (size_t)round_up(c->cp_max_rows, 16) * c->NB) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        set_err(c, "cudaMalloc of the combined panel failed");
+        return HPL_ERR_OOM;
+    }
     return HPL_OK;
 }
 
@@ -1104,6 +1162,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
     else if (!strcmp(name, "store_l")) c->store_l = value != 0;
+    else if (!strcmp(name, "fact_gather")) c->fact_gather_rows = std::max<int64_t>(0, value);
     else if (!strcmp(name, "leaf_variant")) {   // process-wide (like the gemm_* knobs)
         if (value < 0 || value > 2) return HPL_ERR_ARG;
         fact_set_leaf_variant((int)value);

@@ -101,6 +101,22 @@ void fact_set_leaf_ctas(int max_ctas, int rows_per_cta);
 // > 0: leaves run as one-warp CTAs (at most this many) that fit next to the
 // trailing DGEMM's CTAs; 0: the multi-warp leaf with fact_set_leaf_ctas' grid
 void fact_set_leaf_warp_ctas(int ctas);
+// Gathered panel FACT (P > 1, small panels): every process of the column
+// builds the combined panel (row c = global row j0 + c) from the packed
+// panels of all P processes (peer memory), factors it with the one-GPU FACT
+// (bitwise the same arithmetic as the distributed leaf), and extracts its own
+// rows.  panel[p] / ld[p] / lrL0[p]: process row p's packed panel of this panel.
+struct FactPeers {
+    const double *panel[MAX_P];
+    long long ld[MAX_P];
+    long long lrL0[MAX_P];
+    int myrow;
+};
+cudaError_t fact_gather(cudaStream_t st, int64_t rows, int64_t jb, int64_t j0, int NB, int P,
+                        const FactPeers &fp, double *Cp, int64_t ldc);
+cudaError_t fact_extract(cudaStream_t st, int64_t mine, int64_t jb, int64_t j0, int NB, int P,
+                         int myrow, int64_t lrL0, const double *Cp, int64_t ldc, double *Pn,
+                         int64_t ldp);
 // Leaf variant of the P = 1 panel FACT: 0 right-looking
 // (default), 1 left-looking, 2 Crout — bitwise-equal results.  P > 1 panels
 // always use the right-looking distributed leaf.

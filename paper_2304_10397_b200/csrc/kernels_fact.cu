@@ -627,6 +627,47 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
     }
 }
 
+// ---------------------------------------------------------------- gathered FACT (P > 1 tail)
+// Combined panel Cp (column-major, ldc): row c = global row j0 + c.  Rows
+// c < jb are the replicated top block T; row c >= jb lives on process row
+// (g / NB) % P at packed-panel row jb + (g2l(g) - lrL0[p]) of that process's
+// panel (column-major, ld ldq[p]), reached through peer memory.
+__global__ void fact_gather_kernel(int rows, int jb, int cols, long long j0, int NB, int P,
+                                   FactPeers fp, double *Cp, long long ldc)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= rows) return;
+    const double *src;
+    long long ld;
+    if (c < jb) {
+        src = fp.panel[fp.myrow] + c;
+        ld = fp.ld[fp.myrow];
+    } else {
+        const long long g = j0 + c;
+        const int p = (int)((g / NB) % P);
+        const long long l = (g / ((long long)NB * P)) * NB + g % NB;
+        src = fp.panel[p] + jb + (l - fp.lrL0[p]);
+        ld = fp.ld[p];
+    }
+    for (int k = blockIdx.y; k < cols; k += gridDim.y) Cp[(long long)k * ldc + c] = __ldcg(src + k * ld);
+}
+
+// This process's packed panel [T; own L rows] <- the factored combined panel.
+__global__ void fact_extract_kernel(int mine, int jb, int cols, long long j0, int NB, int P,
+                                    int myrow, long long lrL0, const double *Cp, long long ldc,
+                                    double *Pn, long long ldp)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;   // packed-panel row
+    if (r >= jb + mine) return;
+    long long c = r;
+    if (r >= jb) {
+        const long long l = lrL0 + (r - jb);
+        const long long g = ((l / NB) * P + myrow) * NB + l % NB;
+        c = g - j0;
+    }
+    for (int k = blockIdx.y; k < cols; k += gridDim.y) Pn[(long long)k * ldp + r] = Cp[(long long)k * ldc + c];
+}
+
 int g_num_sms = 0;
 int g_leaf_max_ctas = 0;        // 0 = all SMs
 int g_leaf_rows_per_cta = 512;
@@ -804,6 +845,28 @@ void fact_work_free(FactWork *w)
     w->cand = nullptr;
     w->bar = nullptr;
     w->info = nullptr;
+}
+
+cudaError_t fact_gather(cudaStream_t st, int64_t rows, int64_t jb, int64_t j0, int NB, int P,
+                        const FactPeers &fp, double *Cp, int64_t ldc)
+{
+    if (rows <= 0) return cudaSuccess;
+    dim3 grid((unsigned)cdiv(rows, 256), (unsigned)std::min<int64_t>(jb, 64));
+    fact_gather_kernel<<<grid, 256, 0, st>>>((int)rows, (int)jb, (int)jb, j0, NB, P, fp, Cp, ldc);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t fact_extract(cudaStream_t st, int64_t mine, int64_t jb, int64_t j0, int NB, int P,
+                         int myrow, int64_t lrL0, const double *Cp, int64_t ldc, double *Pn,
+                         int64_t ldp)
+{
+    if (jb + mine <= 0) return cudaSuccess;
+    dim3 grid((unsigned)cdiv(jb + mine, 256), (unsigned)std::min<int64_t>(jb, 64));
+    fact_extract_kernel<<<grid, 256, 0, st>>>((int)mine, (int)jb, (int)jb, j0, NB, P, myrow, lrL0,
+                                              Cp, ldc, Pn, ldp);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t panel_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t ldp,

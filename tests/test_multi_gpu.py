@@ -140,3 +140,19 @@ def test_peer_exchange_two_factorizations():
         pytest.skip("needs 4 GPUs")
     out = _run(4, 2048, 64, 2, 2, ("--repeat", "2"))
     assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
+
+
+@pytest.mark.parametrize("P,Q", [(2, 1), (2, 2)])
+def test_gathered_fact_vs_distributed(P, Q):
+    """P > 1 panel FACT two ways: the distributed leaf (one NVLink pivot
+    exchange per column, fact_gather=0) and the gathered FACT (every process
+    of the column factors the combined panel; the default for panels of at most
+    32768 global rows).  Both give the oracle's pivots and x within 1e-9, and
+    the same x (same arithmetic), also with a threshold that switches mode
+    mid-run."""
+    if _ngpu() < P * Q:
+        pytest.skip(f"needs {P * Q} GPUs")
+    outs = [_run(P * Q, 3000, 128, P, Q, (f"--opt=fact_gather={g}",)) for g in (0, 1 << 20, 1500)]
+    for o in outs:
+        assert o["ipiv_equal"] and o["x_rel"] <= 1e-9 and o["resid"] < 16, o
+    assert outs[0]["x_rel"] == outs[1]["x_rel"] == outs[2]["x_rel"]
