@@ -1162,6 +1162,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
     else if (!strcmp(name, "store_l")) c->store_l = value != 0;
+    else if (!strcmp(name, "leaf_cluster")) fact_set_leaf_cluster((int)value);   // process-wide
     else if (!strcmp(name, "fact_gather")) c->fact_gather_rows = std::max<int64_t>(0, value);
     else if (!strcmp(name, "leaf_variant")) {   // process-wide (like the gemm_* knobs)
         if (value < 0 || value > 2) return HPL_ERR_ARG;

@@ -121,6 +121,9 @@ cudaError_t fact_extract(cudaStream_t st, int64_t mine, int64_t jb, int64_t j0, 
 // (default), 1 left-looking, 2 Crout — bitwise-equal results.  P > 1 panels
 // always use the right-looking distributed leaf.
 void fact_set_leaf_variant(int v);
+// Small panels (<= 16 x 1664 rows) use the one-cluster shared-memory leaf
+// (DSMEM candidates, hardware cluster barrier); 0 = always the grid leaf.
+void fact_set_leaf_cluster(int on);
 int fact_get_leaf_variant();
 // Pivot winner among n candidates (max |v|, ties -> smallest row), as the FACT reduces.
 cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,

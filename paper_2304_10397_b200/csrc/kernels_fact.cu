@@ -13,6 +13,7 @@
 // applies the swap to the rows it owns and updates them.  The recursion's
 // TRSM and GEMM steps run as separate kernels (the GEMM is the DMMA kernel).
 #include "hpl_internal.cuh"
+#include <cooperative_groups.h>
 #include <cstdio>
 
 namespace hpl {
@@ -627,6 +628,141 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
     }
 }
 
+// ---------------------------------------------------------------- cluster leaf (small panels)
+// For panels of at most CL_SIZE x CL_ROWS rows (the tail, where FACT is on the
+// critical path): ONE thread-block cluster factors the leaf with its w
+// columns resident in shared memory (CL_ROWS rows per CTA), the candidate
+// records written into every CTA's shared memory through DSMEM and one
+// hardware cluster barrier per column — no L2 round trips per column, no
+// grid-wide software barrier.  Same candidate rule and the same per-row
+// operations as leaf_fact_kernel (bitwise-equal results, tested).
+namespace cg = cooperative_groups;
+constexpr int CL_SIZE = 16;           // non-portable cluster size (B200 allows 16)
+constexpr int CL_THREADS = 512;
+constexpr int CL_ROWS = 1664;         // rows per CTA: 1664 x 16 x 8 B = 208 KB of slab
+
+__global__ void __launch_bounds__(CL_THREADS, 1)
+leaf_fact_cluster_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv,
+                         unsigned long long *info, long long goff, int chunk)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int CS = (int)cl.num_blocks();
+    extern __shared__ double slab[];                 // slab[c * chunk + r]
+    __shared__ double recs[2][CL_SIZE][REC];         // (|v|, row, row's leaf values) per CTA
+    __shared__ double rowk[2][LEAF_MAX];             // row kc's leaf values (from its owner)
+    __shared__ double s_v[CL_THREADS / 32];
+    __shared__ long long s_r[CL_THREADS / 32];
+    __shared__ double s_prow[LEAF_MAX], s_rowk[LEAF_MAX];
+    __shared__ long long s_p;
+    __shared__ double s_piv;
+    const int tid = threadIdx.x;
+    const int rbeg = k0 + rank * chunk;
+    const int rend = min(m, rbeg + chunk);
+    const int nr = max(0, rend - rbeg);
+    for (int c = 0; c < w; ++c)
+        for (int r = tid; r < nr; r += CL_THREADS)
+            slab[c * chunk + r] = P[(int64_t)(k0 + c) * ldp + rbeg + r];
+    __syncthreads();
+    double bv = -1.0;
+    long long br = LLONG_MAX;
+    for (int r = tid; r < nr; r += CL_THREADS) {
+        const double v = fabs(slab[r]);
+        if (better(v, rbeg + r, bv, br)) { bv = v; br = rbeg + r; }
+    }
+    for (int kk = 0; kk < w; ++kk) {
+        const int kc = k0 + kk, par = kk & 1;
+        // ---- 1. this CTA's candidate, written into every CTA of the cluster
+        warp_argmax(bv, br);
+        if ((tid & 31) == 0) { s_v[tid >> 5] = bv; s_r[tid >> 5] = br; }
+        __syncthreads();
+        if (tid < 32) {
+            bv = tid < CL_THREADS / 32 ? s_v[tid] : -1.0;
+            br = tid < CL_THREADS / 32 ? s_r[tid] : LLONG_MAX;
+            warp_argmax(bv, br);
+            // lanes write the record's words to every destination CTA
+            for (int e = tid; e < CS * (2 + LEAF_MAX); e += 32) {
+                const int dst = e / (2 + LEAF_MAX), q = e % (2 + LEAF_MAX);
+                double val;
+                if (q == 0) val = bv;
+                else if (q == 1) val = __longlong_as_double(br);
+                else val = (br != LLONG_MAX && q - 2 < w) ? slab[(q - 2) * chunk + (br - rbeg)] : 0.0;
+                double *d = cl.map_shared_rank(&recs[par][rank][q], dst);
+                *d = val;
+            }
+            if (kc >= rbeg && kc < rend)
+                for (int e = tid; e < CS * LEAF_MAX; e += 32) {
+                    const int dst = e / LEAF_MAX, q = e % LEAF_MAX;
+                    double *d = cl.map_shared_rank(&rowk[par][q], dst);
+                    *d = q < w ? slab[q * chunk + (kc - rbeg)] : 0.0;
+                }
+        }
+        cl.sync();
+        // ---- 2. every CTA reduces the CS records (same order: same winner)
+        if (tid < 32) {
+            bv = -1.0;
+            br = LLONG_MAX;
+            int bc = -1;
+            if (tid < CS) {
+                const double v = recs[par][tid][0];
+                const long long r = __double_as_longlong(recs[par][tid][1]);
+                if (r != LLONG_MAX) { bv = v; br = r; bc = tid; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
+            }
+            if (tid == 0) { s_p = br; s_piv = recs[par][bc][2 + kk]; }
+            if (tid < w) {
+                s_prow[tid] = recs[par][bc][2 + tid];
+                s_rowk[tid] = rowk[par][tid];
+            }
+        }
+        __syncthreads();
+        const long long p = s_p;
+        const double piv = s_piv;
+        if (tid == 0 && rank == 0) {
+            ipiv[kc] = p;
+            if (piv == 0.0) atomicMin(info, (unsigned long long)(goff + kc));
+        }
+        // ---- 3. swap rows kc and p inside the leaf columns (owners)
+        if (p != kc) {
+            if (kc >= rbeg && kc < rend && tid < w) slab[tid * chunk + (kc - rbeg)] = s_prow[tid];
+            if (p >= rbeg && p < rend && tid < w) slab[tid * chunk + (p - rbeg)] = s_rowk[tid];
+        }
+        __syncthreads();
+        // ---- 4. scale + rank-1 update of own rows > kc; next column's candidate
+        bv = -1.0;
+        br = LLONG_MAX;
+        for (int r = max(0, kc + 1 - rbeg) + tid; r < nr; r += CL_THREADS) {
+            const double xk = slab[kk * chunk + r];
+            const double l = xk / piv;
+            slab[kk * chunk + r] = l;
+            double nv = 0.0;
+#pragma unroll
+            for (int c = 0; c < LEAF_MAX; ++c) {
+                const int cc = kk + 1 + c;
+                if (cc < w) {
+                    const double v = fma(-l, s_prow[cc], slab[cc * chunk + r]);
+                    slab[cc * chunk + r] = v;
+                    if (c == 0) nv = fabs(v);
+                }
+            }
+            if (kk + 1 < w && better(nv, rbeg + r, bv, br)) { bv = nv; br = rbeg + r; }
+        }
+        __syncthreads();
+    }
+    for (int c = 0; c < w; ++c)
+        for (int r = tid; r < nr; r += CL_THREADS)
+            P[(int64_t)(k0 + c) * ldp + rbeg + r] = slab[c * chunk + r];
+    cl.sync();   // no CTA leaves while a peer could still address its shared memory
+}
+
+int g_leaf_cluster = 1;         // cluster leaf for panels of <= CL_SIZE * CL_ROWS rows
+
 // ---------------------------------------------------------------- gathered FACT (P > 1 tail)
 // Combined panel Cp (column-major, ldc): row c = global row j0 + c.  Rows
 // c < jb are the replicated top block T; row c >= jb lives on process row
@@ -697,6 +833,43 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int 
         int dev;
         HPL_CUDA_TRY(cudaGetDevice(&dev));
         HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (g_leaf_cluster && g_leaf_variant == 0 && g_leaf_warp_ctas == 0 &&
+        m - k0 <= (int64_t)CL_SIZE * CL_ROWS && w <= LEAF_MAX && w > 0 && m - k0 > 0) {
+        const int chunk = (int)cdiv(m - k0, CL_SIZE);
+        const size_t smem = sizeof(double) * (size_t)chunk * w;
+        static bool attr = false;
+        if (!attr) {
+            HPL_CUDA_TRY(cudaFuncSetAttribute(leaf_fact_cluster_kernel,
+                                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            HPL_CUDA_TRY(cudaFuncSetAttribute(leaf_fact_cluster_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)(sizeof(double) * CL_ROWS * LEAF_MAX)));
+            attr = true;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(CL_SIZE);
+        cfg.blockDim = dim3(CL_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL_SIZE;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, leaf_fact_cluster_kernel, (int)m, ldp, P,
+                                                 k0, w, ipiv,
+                                                 reinterpret_cast<unsigned long long *>(wk->info),
+                                                 goff, chunk);
+        if (e == cudaSuccess) {
+            count_launch();
+            return cudaSuccess;
+        }
+        // a device that cannot place a 16-CTA cluster: the grid leaf from now on
+        cudaGetLastError();
+        g_leaf_cluster = 0;
     }
     int G, NT;
     leaf_grid(m - k0, wk->max_ctas, &G, &NT);
@@ -812,6 +985,7 @@ cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64
 
 void fact_set_leaf_warp_ctas(int ctas) { g_leaf_warp_ctas = ctas; }
 void fact_set_leaf_variant(int v) { g_leaf_variant = (v >= 0 && v <= 2) ? v : 0; }
+void fact_set_leaf_cluster(int on) { g_leaf_cluster = on ? 1 : 0; }
 int fact_get_leaf_variant() { return g_leaf_variant; }
 
 void fact_set_leaf_ctas(int max_ctas, int rows_per_cta)

@@ -136,6 +136,42 @@ def test_leaf_variant_end_to_end(H):
         assert np.array_equal(p, p0) and np.array_equal(x, x0) and r < 16
 
 
+@pytest.mark.parametrize("m,nb,nbmin", [(5000, 128, 16), (777, 64, 16), (26624, 256, 16),
+                                        (26625, 64, 16), (300, 33, 8), (40, 40, 16),
+                                        (20000, 512, 16)])
+def test_panel_fact_cluster_leaf(H, m, nb, nbmin):
+    """The one-cluster shared-memory leaf (panels <= 16 x 1664 rows, default)
+    against the oracle and bitwise against the grid leaf (leaf_cluster=0)."""
+    Pn = hpl_panel(m, nb, seed=7 * m + nb)
+    LU1, ip1, info1 = H.hplk_panel_fact(Pn, nbmin=nbmin)
+    with H.hpl_init(64, 16, 1, 1, 1) as ctx:   # the knob is process-wide
+        H.hpl_set_option(ctx, "leaf_cluster", 0)
+        try:
+            LU0, ip0, info0 = H.hplk_panel_fact(Pn, nbmin=nbmin)
+        finally:
+            H.hpl_set_option(ctx, "leaf_cluster", 1)
+    LUo, ipo, _ = oracle.getrf(Pn)
+    assert info1 == -1 and info0 == -1 and np.array_equal(ip1, ipo)
+    assert np.max(np.abs(LU1 - LUo)) <= 1e-12
+    assert np.array_equal(ip1, ip0) and np.array_equal(LU1, LU0)
+
+
+def test_cluster_leaf_end_to_end(H):
+    """A whole solve with the grid leaf only vs the default (cluster leaf for
+    small panels): pivots and x bitwise equal."""
+    def run(v):
+        with H.hpl_init(6000, 256, 1, 1, 37) as ctx:
+            H.hpl_set_option(ctx, "leaf_cluster", v)
+            try:
+                H.hpl_factor(ctx)
+                return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+            finally:
+                H.hpl_set_option(ctx, "leaf_cluster", 1)
+    xa, pa, _ = run(0)
+    xb, pb, rb = run(1)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
+
+
 def test_panel_fact_special(H):
     LU, ipiv, info = H.hplk_panel_fact(np.array([[0.0], [3.0]]), nbmin=1)
     assert list(ipiv) == [1] and LU[0, 0] == 3.0 and LU[1, 0] == 0.0 and info == -1
