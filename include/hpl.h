@@ -138,6 +138,8 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *                          are factored whole on every GPU of the process column
  *                          (gathered over peer memory) instead of by the
  *                          distributed leaf; 0 = always distributed
+ *   leaf_cluster 0|1 (1)   small panels (<= 16 x 1664 rows) factored by one 16-CTA
+ *                          cluster with the leaf in shared memory (process-wide)
  *   leaf_variant 0|1|2 (0) P=1 FACT leaf: right-looking / left-looking / Crout
  *                          (bitwise-equal results; process-wide)
  *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas, leaf_rows   leaf grid policy
