@@ -14,11 +14,13 @@
 // the trailing update runs on S_tr; events order the two.
 //
 // Distribution: 2D block-cyclic over P x Q (rank = p + q*P).
-// This revision drives 1 x Q grids: FACT runs on the process column that owns
-// panel j, and the packed panel (with its pivots) is broadcast along the
-// process row (LBCAST: "Processes which do not participate
-// in the FACT phase simply wait in the LBCAST phase").  P > 1 (pivot
-// exchange and RS along process columns) is rejected with HPL_ERR_ARG.
+// FACT runs on the process column that owns panel j (P > 1: pivot exchange
+// inside the leaf over peer memory, or the gathered FACT for small panels);
+// the packed panel (with its pivots) reaches the process row by a copy-engine
+// pull over peer memory (LBCAST: "Processes which do not
+// participate in the FACT phase simply wait in the LBCAST phase"); the row
+// swaps cross process rows as a peer-memory gather (RS).  NCCL carries the
+// setup, the replicated top block, the back solve and the residual.
 #include "hpl_internal.cuh"
 #include "../../include/hpl.h"
 #include <nccl.h>
