@@ -145,6 +145,8 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas, leaf_rows   leaf grid policy
  *   gemm_cfg, gemm_tpc, gemm_red   DGEMM tile config / tiles per CTA / RED epilogue
  *   early_next 0|1 (0)     update panel j+2's columns first inside rest(j)
+ *   store_l 0|1 (1)        write L21 back into A (the solve needs only U and y)
+ *   la_below_rs 0|1 (0)    look-ahead stream one priority level below RS/DTRSM
  * Unknown names return HPL_ERR_ARG.  On a multi-process context every rank
  * must set the same options before the same hpl_factor (the schedule decides
  * which collectives and peer-memory barriers are issued). */

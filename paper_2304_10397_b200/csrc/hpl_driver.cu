@@ -94,6 +94,7 @@ struct hpl_ctx {
     double *x = nullptr, *tbuf = nullptr, *out4 = nullptr;
     FactWork fw{};
     cudaStream_t s_la = nullptr, s_tr = nullptr;
+    cudaStream_t s_la_hi = nullptr, s_la_mid = nullptr;   // s_la is one of these
     cudaEvent_t ev_panel[NBUF] = {}, ev_rest = nullptr;
     cudaEvent_t ev_next = nullptr;   // rest(j) has updated panel j+2's columns
     cudaEvent_t ev_trsm = nullptr;   // rest(j)'s LASWP+DTRSM done: FACT(j+1) may start
@@ -516,6 +517,10 @@ hpl_status alloc_ctx(hpl_ctx *c)
     int lo, hi;
     CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(c, cudaStreamCreateWithPriority(&c->s_la, cudaStreamNonBlocking, hi));
+    // the look-ahead stream one level below S_rs (option la_below_rs)
+    CK(c, cudaStreamCreateWithPriority(&c->s_la_mid, cudaStreamNonBlocking,
+                                       hi < lo ? hi + 1 : hi));
+    c->s_la_hi = c->s_la;
     CK(c, cudaStreamCreateWithPriority(&c->s_tr, cudaStreamNonBlocking, lo));
     CK(c, cudaStreamCreateWithPriority(&c->s_rs, cudaStreamNonBlocking, hi));
     for (cudaEvent_t *e : {&c->ev_rsR, &c->ev_rsL, &c->ev_dgR, &c->ev_dgL})
@@ -576,7 +581,8 @@ void release(hpl_ctx *c)
     for (auto e : c->tev) cudaEventDestroy(e);
     for (int k = 0; k < 3; ++k)
         if (c->ev_t[k]) cudaEventDestroy(c->ev_t[k]);
-    if (c->s_la) cudaStreamDestroy(c->s_la);
+    if (c->s_la_hi) cudaStreamDestroy(c->s_la_hi);
+    if (c->s_la_mid) cudaStreamDestroy(c->s_la_mid);
     if (c->s_tr) cudaStreamDestroy(c->s_tr);
 }
 
@@ -1164,6 +1170,10 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     else if (!strcmp(name, "hp_trsm")) c->hp_trsm = value != 0;
     else if (!strcmp(name, "rs_peer")) c->rs_peer = value != 0 && c->rsflag != nullptr;
     else if (!strcmp(name, "store_l")) c->store_l = value != 0;
+    else if (!strcmp(name, "la_below_rs")) {     // between factorizations only
+        cudaStreamSynchronize(c->s_la);
+        c->s_la = value ? c->s_la_mid : c->s_la_hi;
+    }
     else if (!strcmp(name, "leaf_cluster")) fact_set_leaf_cluster((int)value);   // process-wide
     else if (!strcmp(name, "fact_gather")) c->fact_gather_rows = std::max<int64_t>(0, value);
     else if (!strcmp(name, "leaf_variant")) {   // process-wide (like the gemm_* knobs)

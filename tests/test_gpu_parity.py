@@ -300,6 +300,19 @@ def test_dgemm_epilogue_variants_bitwise(H, epi):
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
 
 
+def test_stream_priority_invariance(H):
+    """The look-ahead stream one priority level below the RS/DTRSM stream
+    (option la_below_rs) only reorders concurrent kernels: bitwise equal."""
+    def run(v):
+        with H.hpl_init(4096, 256, 1, 1, 41) as ctx:
+            H.hpl_set_option(ctx, "la_below_rs", v)
+            H.hpl_factor(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+    xa, pa, _ = run(0)
+    xb, pb, rb = run(1)
+    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
+
+
 def test_trsm_pipe_invariance(H):
     """DTRSM / DGEMM pipelined over column chunks (option trsm_pipe; active
     while the trailing width >= 8192) moves no arithmetic between columns:
