@@ -134,10 +134,12 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *   hp_trsm 0|1 (1)        rest LASWP + DTRSM on the high-priority stream
  *   trsm_pipe <k> (1)      DTRSM/DGEMM of the rest pipelined over k column chunks
  *   nbmin <1..16> (16)     recursion base width of the panel FACT
- *   fact_gather <rows> (32768)  P>1: panels with at most this many global rows
- *                          are factored whole on every GPU of the process column
- *                          (gathered over peer memory) instead of by the
- *                          distributed leaf; 0 = always distributed
+ *   fact_gather <rows> (65536), fact_gather_ms <ms> (8)  P>1: a panel with at
+ *                          most this many global rows whose per-GPU trailing
+ *                          update is estimated below fact_gather_ms (FACT on the
+ *                          critical path) is factored whole on every GPU of the
+ *                          process column (gathered over peer memory) instead of
+ *                          by the distributed leaf; fact_gather 0 = never
  *   leaf_cluster 0|1 (1)   small panels (<= 16 x 1664 rows) factored by one 16-CTA
  *                          cluster with the leaf in shared memory (process-wide)
  *   leaf_variant 0|1|2 (0) P=1 FACT leaf: right-looking / left-looking / Crout

@@ -61,7 +61,9 @@ struct hpl_ctx {
     const double *colpanel[MAX_P][3] = {};
     double *Cp = nullptr;            // combined panel, cp_max_rows x NB (col-major)
     int64_t cp_max_rows = 0;
-    int64_t fact_gather_rows = 32768;
+    int64_t fact_gather_rows = 65536;   // at most this many global rows, and
+    double fact_gather_ms = 8.0;        // only where the trailing update is short
+                                        // (FACT on the critical path)
     unsigned long long fg_seq = 0;
     // Q > 1 LBCAST over peer memory (option lb_peer, default on): the panel
     // buffers and LBCAST flags of every process column, IPC-mapped inside the
@@ -219,7 +221,12 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
                             cudaMemcpyDeviceToDevice, st));
     CK(c, rm_to_cm(st, mL, jb, c->A + lrL0 * c->lda + lcp, c->lda, c->panel[b] + jb, ldpj));
     const int64_t rows_total = c->N - j0;   // T + every process row's L rows
-    if (c->fact_gather_rows > 0 && rows_total <= std::min(c->fact_gather_rows, c->cp_max_rows)) {
+    // decided from global sizes only, so every process of the column agrees:
+    // the per-GPU trailing update this FACT hides behind, at 35 TFLOP/s
+    const double rest_ms = 2.0 * (double)cdiv(rows_total, c->P) * (double)cdiv(rows_total, c->Q) *
+                           (double)c->NB / 35e12 * 1e3;
+    if (c->fact_gather_rows > 0 && rows_total <= std::min(c->fact_gather_rows, c->cp_max_rows) &&
+        rest_ms <= c->fact_gather_ms) {
         // Gathered FACT: barrier (every packed panel of the column is ready),
         // build the combined panel from peer memory, barrier (every peer has
         // read this panel), factor it here (the same arithmetic the
@@ -1176,6 +1183,7 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
     }
     else if (!strcmp(name, "leaf_cluster")) fact_set_leaf_cluster((int)value);   // process-wide
     else if (!strcmp(name, "fact_gather")) c->fact_gather_rows = std::max<int64_t>(0, value);
+    else if (!strcmp(name, "fact_gather_ms")) c->fact_gather_ms = (double)value;
     else if (!strcmp(name, "leaf_variant")) {   // process-wide (like the gemm_* knobs)
         if (value < 0 || value > 2) return HPL_ERR_ARG;
         fact_set_leaf_variant((int)value);

@@ -146,8 +146,8 @@ def test_peer_exchange_two_factorizations():
 def test_gathered_fact_vs_distributed(P, Q):
     """P > 1 panel FACT two ways: the distributed leaf (one NVLink pivot
     exchange per column, fact_gather=0) and the gathered FACT (every process
-    of the column factors the combined panel; the default for panels of at most
-    32768 global rows).  Both give the oracle's pivots and x within 1e-9, and
+    of the column factors the combined panel; the default for small panels
+    whose trailing update is short).  Both give the oracle's pivots and x within 1e-9, and
     the same x (same arithmetic), also with a threshold that switches mode
     mid-run."""
     if _ngpu() < P * Q:
