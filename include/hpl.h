@@ -161,6 +161,15 @@ int64_t hpl_launch_count(const hpl_ctx *ctx);
  * kernel launches}.  The DGEMM entries are filled only with hpl_set_timing(1). */
 hpl_status hpl_last_timing(const hpl_ctx *ctx, double *out6);
 
+/* Host-only bookkeeping of the P > 1 panel FACT of panel j on process row
+ * myrow (DESIGN.md §6 "Gathered panel FACT"):
+ * out5 = {mode (-1: P = 1, 0: distributed leaf, 1: gathered — a function of
+ * the global sizes only, identical on every process row), global rows of the
+ * panel N - j*NB, first local L row, number of local L rows, leading
+ * dimension of the packed [T; L] panel}.  gather_rows / gather_ms as the
+ * fact_gather / fact_gather_ms options.  HPL_ERR_ARG on invalid arguments. */
+hpl_status hpl_plan_fact(int64_t N, int32_t NB, int32_t P, int32_t Q, int32_t myrow, int64_t j,
+                         int64_t gather_rows, double gather_ms, int64_t *out5);
 /* Host-only planning of iteration j for process (myrow, mycol) of a P x Q
  * grid (no GPU work; the factor loop uses the same bookkeeping):
  * out8 = {first active local row, first trailing local column, look-ahead

@@ -56,6 +56,7 @@ _sig("hpl_set_option", ctypes.c_int, [ctx_p, ctypes.c_char_p, i64])
 _sig("hpl_launch_count", i64, [ctx_p])
 _sig("hpl_last_timing", ctypes.c_int, [ctx_p, vp])
 _sig("hpl_plan_iteration", ctypes.c_int, [i64, i32, i32, i32, i32, i32, i64, vp])
+_sig("hpl_plan_fact", ctypes.c_int, [i64, i32, i32, i32, i32, i64, i64, ctypes.c_double, vp])
 _sig("hpl_pin_host", ctypes.c_int, [vp, i64, i32])
 
 # ---- include/hpl_kernels.h
@@ -75,7 +76,7 @@ EXPORTED = [
     "hpl_residual", "hpl_regenerate", "hpl_load_local", "hpl_local_shape", "hpl_free",
     "hpl_last_error", "hpl_singular_column", "hpl_get_ipiv", "hpl_get_local",
     "hpl_get_timeline", "hpl_get_fact_detail", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
-    "hpl_last_timing", "hpl_plan_iteration", "hpl_pin_host",
+    "hpl_last_timing", "hpl_plan_iteration", "hpl_plan_fact", "hpl_pin_host",
     "hplk_dgemm_update", "hplk_trsm", "hplk_panel_fact", "hplk_laswp", "hplk_back_solve",
     "hplk_generate", "hplk_maxloc", "hplk_dgemm_bench", "hplk_dmma_peak", "hplk_panel_bench",
 ]

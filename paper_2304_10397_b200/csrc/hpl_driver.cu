@@ -195,6 +195,20 @@ int64_t *panel_ipiv(hpl_ctx *c, int64_t j, int b)
     return reinterpret_cast<int64_t *>(c->panel[b] + jb_of(c, j) * panel_ld(c, j));
 }
 
+// P > 1: factor panel j gathered (true) or with the distributed leaf.  Global
+// sizes only, so every process of the column takes the same path (the two
+// paths issue different peer-memory barriers).
+bool use_gathered_fact(int64_t N, int NB, int P, int Q, int64_t j, int64_t gather_rows,
+                       double gather_ms, int64_t cp_max_rows)
+{
+    if (P < 2 || gather_rows <= 0) return false;
+    const int64_t rows_total = N - j * NB;   // T + every process row's L rows
+    // the per-GPU trailing update this FACT hides behind, at 35 TFLOP/s
+    const double rest_ms = 2.0 * (double)cdiv(rows_total, P) * (double)cdiv(rows_total, Q) *
+                           (double)NB / 35e12 * 1e3;
+    return rows_total <= std::min(gather_rows, cp_max_rows) && rest_ms <= gather_ms;
+}
+
 // FACT(j) on the process column that owns panel j: pack [T; L] column-major,
 // factor, write the factored panel back to A.
 hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
@@ -221,12 +235,8 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
                             cudaMemcpyDeviceToDevice, st));
     CK(c, rm_to_cm(st, mL, jb, c->A + lrL0 * c->lda + lcp, c->lda, c->panel[b] + jb, ldpj));
     const int64_t rows_total = c->N - j0;   // T + every process row's L rows
-    // decided from global sizes only, so every process of the column agrees:
-    // the per-GPU trailing update this FACT hides behind, at 35 TFLOP/s
-    const double rest_ms = 2.0 * (double)cdiv(rows_total, c->P) * (double)cdiv(rows_total, c->Q) *
-                           (double)c->NB / 35e12 * 1e3;
-    if (c->fact_gather_rows > 0 && rows_total <= std::min(c->fact_gather_rows, c->cp_max_rows) &&
-        rest_ms <= c->fact_gather_ms) {
+    if (use_gathered_fact(c->N, c->NB, c->P, c->Q, j, c->fact_gather_rows, c->fact_gather_ms,
+                          c->cp_max_rows)) {
         // Gathered FACT: barrier (every packed panel of the column is ready),
         // build the combined panel from peer memory, barrier (every peer has
         // read this panel), factor it here (the same arithmetic the
@@ -1197,6 +1207,26 @@ hpl_status hpl_set_option(hpl_ctx *c, const char *name, int64_t value)
 }
 
 int64_t hpl_launch_count(const hpl_ctx *c) { return c ? c->launches : 0; }
+
+hpl_status hpl_plan_fact(int64_t N, int32_t NB, int32_t P, int32_t Q, int32_t myrow, int64_t j,
+                         int64_t gather_rows, double gather_ms, int64_t *out5)
+{
+    if (!out5 || N < 1 || NB < 1 || P < 1 || Q < 1 || myrow < 0 || myrow >= P || j < 0 ||
+        j * NB >= N)
+        return HPL_ERR_ARG;
+    hpl_ctx t;
+    t.N = N; t.NB = NB; t.P = P; t.Q = Q; t.myrow = myrow;
+    t.mloc = numroc(N, NB, myrow, P);
+    const int64_t jb = jb_of(&t, j), lrL0 = lrL0_of(&t, j), mL = t.mloc - lrL0;
+    out5[0] = P < 2 ? -1
+                    : use_gathered_fact(N, NB, P, Q, j, gather_rows, gather_ms,
+                                        std::min<int64_t>(N, (int64_t)1 << 16)) ? 1 : 0;
+    out5[1] = N - j * NB;                   // global rows of the panel (T + all L rows)
+    out5[2] = lrL0;                         // this process row's first L row (local)
+    out5[3] = mL;                           // this process row's L rows
+    out5[4] = panel_ld(&t, j);              // leading dimension of its packed panel
+    return HPL_OK;
+}
 
 hpl_status hpl_plan_iteration(int64_t N, int32_t NB, int32_t P, int32_t Q, int32_t myrow,
                               int32_t mycol, int64_t j, int64_t *out8)

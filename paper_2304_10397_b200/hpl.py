@@ -183,6 +183,17 @@ def hpl_plan_iteration(N: int, NB: int, P: int, Q: int, myrow: int, mycol: int, 
                 lpanel=int(o[6]), jb=int(o[7]))
 
 
+def hpl_plan_fact(N: int, NB: int, P: int, Q: int, myrow: int, j: int,
+                  gather_rows: int = 65536, gather_ms: float = 8.0) -> dict:
+    """Host-only bookkeeping of panel j's FACT on process row myrow (P > 1:
+    distributed leaf or gathered FACT, decided from global sizes)."""
+    o = np.zeros(5, dtype=np.int64)
+    st = lib.hpl_plan_fact(N, NB, P, Q, myrow, j, gather_rows, float(gather_ms), ptr(o))
+    if st != 0:
+        raise HplError(st, "hpl_plan_fact: invalid arguments")
+    return dict(mode=int(o[0]), rows=int(o[1]), lrL0=int(o[2]), mL=int(o[3]), ldp=int(o[4]))
+
+
 def hpl_pin_host(arr: np.ndarray, pin: bool = True) -> bool:
     """Page-lock a host array for DMA-speed copies; returns False if refused."""
     return lib.hpl_pin_host(ptr(arr), arr.nbytes, 1 if pin else 0) == 0
