@@ -195,6 +195,18 @@ int64_t *panel_ipiv(hpl_ctx *c, int64_t j, int b)
     return reinterpret_cast<int64_t *>(c->panel[b] + jb_of(c, j) * panel_ld(c, j));
 }
 
+// Packed-panel geometry of process row p for panel j: first local L row,
+// number of local L rows, leading dimension of [T; L] (hpl_plan_fact and the
+// gathered FACT's peer map use this one function).
+void fact_geom(int64_t N, int NB, int P, int p, int64_t j, int64_t *lrL0, int64_t *mL,
+               int64_t *ldp)
+{
+    const int64_t jb = std::min<int64_t>(NB, N - j * NB);
+    *lrL0 = numroc(j * NB, NB, p, P) + ((int)(j % P) == p ? jb : 0);
+    *mL = numroc(N, NB, p, P) - *lrL0;
+    *ldp = round_up(jb + *mL, 16);
+}
+
 // P > 1: factor panel j gathered (true) or with the distributed leaf.  Global
 // sizes only, so every process of the column takes the same path (the two
 // paths issue different peer-memory barriers).
@@ -246,10 +258,10 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
         FactPeers fp{};
         fp.myrow = c->myrow;
         for (int p = 0; p < c->P; ++p) {
-            const int64_t lr0p = numroc(j0, c->NB, p, c->P) + (p == prow_of(c, j) ? jb : 0);
-            const int64_t mLp = numroc(c->N, c->NB, p, c->P) - lr0p;
+            int64_t lr0p, mLp, ldq;
+            fact_geom(c->N, c->NB, c->P, p, j, &lr0p, &mLp, &ldq);
             fp.panel[p] = c->colpanel[p][b];
-            fp.ld[p] = round_up(jb + mLp, 16);
+            fp.ld[p] = ldq;
             fp.lrL0[p] = lr0p;
         }
         const int64_t ldc = round_up(rows_total, 16);
@@ -1214,17 +1226,15 @@ hpl_status hpl_plan_fact(int64_t N, int32_t NB, int32_t P, int32_t Q, int32_t my
     if (!out5 || N < 1 || NB < 1 || P < 1 || Q < 1 || myrow < 0 || myrow >= P || j < 0 ||
         j * NB >= N)
         return HPL_ERR_ARG;
-    hpl_ctx t;
-    t.N = N; t.NB = NB; t.P = P; t.Q = Q; t.myrow = myrow;
-    t.mloc = numroc(N, NB, myrow, P);
-    const int64_t jb = jb_of(&t, j), lrL0 = lrL0_of(&t, j), mL = t.mloc - lrL0;
+    int64_t lrL0, mL, ldp;
+    fact_geom(N, NB, P, myrow, j, &lrL0, &mL, &ldp);
     out5[0] = P < 2 ? -1
                     : use_gathered_fact(N, NB, P, Q, j, gather_rows, gather_ms,
                                         std::min<int64_t>(N, (int64_t)1 << 16)) ? 1 : 0;
     out5[1] = N - j * NB;                   // global rows of the panel (T + all L rows)
     out5[2] = lrL0;                         // this process row's first L row (local)
     out5[3] = mL;                           // this process row's L rows
-    out5[4] = panel_ld(&t, j);              // leading dimension of its packed panel
+    out5[4] = ldp;                          // leading dimension of its packed panel
     return HPL_OK;
 }
 
