@@ -1,5 +1,5 @@
-"""Multi-process host logic on CPU (gloo, world_size 2 and 4): the per-rank
-iteration plan of the 1 x Q / P x Q block-cyclic driver (hpl_plan_iteration,
+"""Multi-process host logic on CPU (gloo, world_size 2, 4 and 8 — the last is
+the 2 x 4 grid of BASELINE.json C4): the per-rank iteration plan of the 1 x Q / P x Q block-cyclic driver (hpl_plan_iteration,
 the same bookkeeping hpl_factor uses) partitions the trailing columns exactly
 and the bench's unique-id exchange round-trips.  No GPU work."""
 import os
@@ -58,7 +58,7 @@ def _worker(rank, world, port, cases, P):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,P", [(2, 1), (4, 1), (4, 2)])
+@pytest.mark.parametrize("world,P", [(2, 1), (4, 1), (4, 2), (8, 2)])
 def test_plan_partitions_trailing_columns(world, P):
     cases = [(1000, 64), (257, 16), (512, 512), (96, 32)]
     mp.spawn(_worker, args=(world, _free_port(), cases, P), nprocs=world, join=True)
