@@ -1,7 +1,8 @@
 """Multi-process host logic on CPU (gloo, world_size 2, 4 and 8 — the last is
-the 2 x 4 grid of BASELINE.json C4): the per-rank iteration plan of the 1 x Q / P x Q block-cyclic driver (hpl_plan_iteration,
-the same bookkeeping hpl_factor uses) partitions the trailing columns exactly
-and the bench's unique-id exchange round-trips.  No GPU work."""
+the 2 x 4 grid of BASELINE.json C4): the per-rank iteration plan of the
+1 x Q / P x Q block-cyclic driver (hpl_plan_iteration, the same bookkeeping
+hpl_factor uses) partitions the trailing columns exactly and the bench's
+unique-id exchange round-trips.  No GPU work."""
 import os
 import socket
 
