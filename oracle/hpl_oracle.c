@@ -193,6 +193,14 @@ int64_t oracle_back_solve(int64_t N, const double *U, int64_t ldu, const double 
     return -1;
 }
 
+/* max for the infinity norms: the norm of a vector with a NaN entry is NaN
+ * (a plain "v > m" would skip it and a NaN solution would pass the check). */
+static double norm_max(double m, double v)
+{
+    if (m != m || v != v) return NAN;
+    return v > m ? v : m;
+}
+
 /* ---------------------------------------------------------------------------
  * O5. HPL scaled residual (BASELINE.json north_star):
  *   resid = ||A0 x - b0||_inf / (eps * (||A0||_inf * ||x||_inf + ||b0||_inf) * N)
@@ -211,10 +219,10 @@ double oracle_residual(int64_t N, const double *A0, int64_t lda, const double *x
             a = a + fabs(A0[i * lda + j]);
         }
         double r = fabs(s - b0[i]);
-        if (r > rinf) rinf = r;
-        if (a > anorm) anorm = a;
-        if (fabs(x[i]) > xnorm) xnorm = fabs(x[i]);
-        if (fabs(b0[i]) > bnorm) bnorm = fabs(b0[i]);
+        rinf = norm_max(rinf, r);
+        anorm = norm_max(anorm, a);
+        xnorm = norm_max(xnorm, fabs(x[i]));
+        bnorm = norm_max(bnorm, fabs(b0[i]));
     }
     const double eps = ldexp(1.0, -53);
     if (out4) { out4[0] = rinf; out4[1] = anorm; out4[2] = xnorm; out4[3] = bnorm; }
@@ -238,19 +246,18 @@ double oracle_residual_seeded(int64_t N, uint64_t seed, const double *x, double 
                 a = a + fabs(v);
             }
             double r = fabs(s - oracle_gen_entry(seed, N, i, N));
-            if (r > lr) lr = r;
-            if (a > la) la = a;
+            lr = norm_max(lr, r);
+            la = norm_max(la, a);
         }
 #pragma omp critical
         {
-            if (lr > rinf) rinf = lr;
-            if (la > anorm) anorm = la;
+            rinf = norm_max(rinf, lr);
+            anorm = norm_max(anorm, la);
         }
     }
     for (int64_t i = 0; i < N; ++i) {
-        if (fabs(x[i]) > xnorm) xnorm = fabs(x[i]);
-        double bi = fabs(oracle_gen_entry(seed, N, i, N));
-        if (bi > bnorm) bnorm = bi;
+        xnorm = norm_max(xnorm, fabs(x[i]));
+        bnorm = norm_max(bnorm, fabs(oracle_gen_entry(seed, N, i, N)));
     }
     const double eps = ldexp(1.0, -53);
     if (out4) { out4[0] = rinf; out4[1] = anorm; out4[2] = xnorm; out4[3] = bnorm; }

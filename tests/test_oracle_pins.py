@@ -262,6 +262,26 @@ def test_residual_closed_forms():
     assert oracle.residual(A, xx, bb)[0] == oracle.residual(A * 2.0 ** 7, xx, bb * 2.0 ** 7)[0]
 
 
+def test_residual_nonfinite_fails():
+    """The infinity norm of a vector with a NaN entry is NaN, not the max of
+    the other entries: a NaN (or inf) anywhere in x makes the scaled residual
+    non-finite, so "resid < 16" fails (a max that skips NaN let
+    a NaN solution pass with resid 0)."""
+    A = np.array([[2.0, 1.0], [1.0, 3.0]])
+    b = A @ np.array([1.0, 2.0])
+    for bad in (np.nan, np.inf, -np.inf):
+        x = np.array([1.0, bad])
+        r, _ = oracle.residual(A, x, b)
+        assert not r < 16.0
+        x = np.array([bad, 2.0])
+        assert not oracle.residual(A, x, b)[0] < 16.0
+    A, b = oracle.generate(3, 40)
+    x = np.linalg.solve(A, b)
+    assert oracle.residual_seeded(40, 3, x)[0] < 16.0
+    x[17] = np.nan
+    assert not oracle.residual_seeded(40, 3, x)[0] < 16.0
+
+
 def test_residual_seeded_matches_explicit():
     A, b = oracle.generate(42, 100)
     x = np.linalg.solve(A, b)
