@@ -21,13 +21,26 @@
  *    with a padded leading dimension.
  *  - Pivots: LAPACK 0-based global row indices (ipiv[k] = row exchanged with
  *    row k at step k); ties -> smallest global row (DESIGN reading A2).
- *  - Threading: a context is not thread-safe.  On a multi-rank context every
- *    call is collective over all P*Q ranks and must be made in the same order.
+ *  - Threading: a context is not thread-safe, but different contexts may be
+ *    driven from different host threads at once (the library keeps no
+ *    process-wide mutable state); the loopback grid (hpl_init_loopback)
+ *    needs exactly that.  On a multi-rank context every call is collective
+ *    over all P*Q ranks and must be made in the same order.
  *  - Call order: init -> factor -> solve -> residual; regenerate / load_local
  *    reset to "initialised".  Out-of-order calls return HPL_ERR_STATE.
  *  - Errors never abort the process: a status is returned and
  *    hpl_last_error() describes it.  CUDA and NCCL failures map to
  *    HPL_ERR_CUDA / HPL_ERR_NCCL; the context should then be freed.
+ *  - Failure detection: every device-side wait on another rank (RS and FACT
+ *    barriers, the pivot exchange, LBCAST flags, collectives) is bounded by
+ *    the peer timeout (option peer_timeout_ms; 60 s, 20 s in a loopback).  A
+ *    rank that dies or does not enter a collective call makes its peers'
+ *    call return HPL_ERR_PEER instead of hanging; the
+ *    context is then broken and must be freed.
+ *  - Argument limits (HPL_ERR_ARG, before any allocation): N >= 1,
+ *    1 <= NB <= N, P, Q >= 1 and the implementation
+ *    limits of DESIGN.md reading A18: NB even and <= 1024, N < 2^31, P <= 8,
+ *    Q <= 32, P*Q <= 32.
  *  - Ownership: the library owns all device memory, streams, events and NCCL
  *    communicators (freed by hpl_free).  Host pointers are caller-owned and
  *    only read/written during the call.
@@ -50,7 +63,8 @@ typedef enum {
     HPL_ERR_OOM = 3,      /* device allocation failed (only at init) */
     HPL_ERR_CUDA = 4,     /* CUDA runtime/driver error */
     HPL_ERR_NCCL = 5,     /* NCCL error */
-    HPL_ERR_SINGULAR = 6  /* exact zero pivot; see hpl_singular_column */
+    HPL_ERR_SINGULAR = 6, /* exact zero pivot; see hpl_singular_column */
+    HPL_ERR_PEER = 7      /* a peer-memory wait timed out: a peer rank failed or is absent */
 } hpl_status;
 
 /* Single-process context on the current CUDA device.  P*Q must be 1.
@@ -74,6 +88,22 @@ hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t s
                          int32_t rank, int32_t nranks, const void *nccl_unique_id,
                          int32_t device, hpl_ctx **out);
 
+/* Single-device P x Q loopback ("ranks are concurrent workers
+ * in one process"): creates the P*Q rank contexts of one grid on CUDA device
+ * `device` of THIS process, out[r] = rank r (r = p + q*P).  They run exactly
+ * the multi-GPU data path — peer-memory RS, pivot exchange, LBCAST flags and
+ * collectives, with the siblings' device pointers in place of IPC mappings —
+ * so one GPU checks it against the oracle.  Each collective call must be made
+ * on every rank concurrently, one host thread per rank.  Because the ranks'
+ * kernels wait on each other, the process must run with
+ * CUDA_MODULE_LOADING=EAGER and CUDA_DEVICE_MAX_CONNECTIONS >= 3*P*Q set
+ * before CUDA initialises (HPL_ERR_STATE otherwise, when P*Q > 1); each
+ * rank's cooperative leaf is capped at SMs/(P*Q) CTAs so all fit at once.
+ * On failure the already-created contexts are still returned in out (free
+ * them).  Free every rank only after all ranks' calls have returned. */
+hpl_status hpl_init_loopback(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t seed,
+                             int32_t device, hpl_ctx **out);
+
 /* Writes a fresh ncclUniqueId (128 bytes) into id_out (rank 0 only). */
 hpl_status hpl_get_unique_id(void *id_out);
 
@@ -88,7 +118,10 @@ hpl_status hpl_solve(hpl_ctx *ctx, double *x_host);
 
 /* HPL scaled residual ||A0 x - b0||_inf / (eps (||A0||_inf ||x||_inf +
  * ||b0||_inf) N), eps = 2^-53 (reading A4), regenerating A0 and b0 from the
- * seed on the fly (the factors are not touched).  Requires hpl_solve. */
+ * seed on the fly (the factors are not touched).  Requires hpl_solve.  A
+ * non-finite x or norm gives +inf (a failed solve never passes "< 16").
+ * After hpl_load_local the factored system is not the seeded one:
+ * HPL_ERR_STATE. */
 hpl_status hpl_residual(hpl_ctx *ctx, double *resid);
 
 /* Refill the local matrix from the seed (returns to the initialised state). */
@@ -126,13 +159,18 @@ int64_t hpl_get_timeline(const hpl_ctx *ctx, double *t, int64_t cap);
 int64_t hpl_get_fact_detail(const hpl_ctx *ctx, double *t, int64_t cap);
 /* Enable per-phase CUDA events (adds a little host work per iteration). */
 hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
-/* Tuning / A-B knobs (none changes the pivots or x; tested):
- *   lookahead 0|1 (1)      look-ahead depth 1 on a high-priority stream
+/* Tuning / A-B knobs (none changes the pivots; each is tested against the
+ * oracle or bitwise against the default in tests/):
+ *   lookahead 0|1 (1)      look-ahead depth 1 on high-priority streams
  *   split <pct> (0)        split update, right-section share
- *   rs_peer 0|1 (1)        P>1 RS over NVLink peer memory; 0 = NCCL all-reduce + broadcast
- *   lb_peer 0|1 (1)        Q>1 LBCAST as copy-engine pulls; 0 = NCCL broadcast
- *   hp_trsm 0|1 (1)        rest LASWP + DTRSM on the high-priority stream
- *   trsm_pipe <k> (1)      DTRSM/DGEMM of the rest pipelined over k column chunks
+ *   rs_peer 0|1 (1)        P>1 RS as a peer-memory row gather; 0 = collective
+ *                          variant (U all-reduced, W broadcast over the column)
+ *   lb_peer 0|1 (1)        Q>1 LBCAST as copy-engine pulls; 0 = broadcast collective
+ *   coll_nccl 0|1 (0)      multi-process: the collectives (replicated top block,
+ *                          back-solve sums/broadcasts, residual norms, rs_peer=0 /
+ *                          lb_peer=0 variants) over NCCL instead of peer memory
+ *                          (NCCL waits are not bounded by peer_timeout_ms)
+ *   peer_timeout_ms <ms>   bound of every device-side wait on a peer (60000)
  *   nbmin <1..16> (16)     recursion base width of the panel FACT
  *   fact_gather <rows> (65536), fact_gather_ms <ms> (8)  P>1: a panel with at
  *                          most this many global rows whose per-GPU trailing
@@ -141,15 +179,12 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *                          process column (gathered over peer memory) instead of
  *                          by the distributed leaf; fact_gather 0 = never
  *   leaf_cluster 0|1 (1)   small panels (<= 16 x 1664 rows) factored by one 16-CTA
- *                          cluster with the leaf in shared memory (process-wide)
+ *                          cluster with the leaf in shared memory
  *   leaf_variant 0|1|2 (0) P=1 FACT leaf: right-looking / left-looking / Crout
- *                          (bitwise-equal results; process-wide)
- *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas, leaf_rows   leaf grid policy
- *   gemm_cfg, gemm_tpc, gemm_red   DGEMM tile config / tiles per CTA / RED epilogue
- *   early_next 0|1 (0)     update panel j+2's columns first inside rest(j)
- *   store_l 0|1 (1)        write L21 back into A (the solve needs only U and y)
- *   la_below_rs 0|1 (0)    look-ahead stream one priority level below RS/DTRSM
- * Unknown names return HPL_ERR_ARG.  On a multi-process context every rank
+ *                          (bitwise-equal results)
+ *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas   leaf grid policy
+ *   gemm_cfg -1|0|1|2 (-1) DGEMM tile config (128x64, 128x128, 64x64 = default)
+ * Every knob is per context.  Unknown names return HPL_ERR_ARG.  On a multi-process context every rank
  * must set the same options before the same hpl_factor (the schedule decides
  * which collectives and peer-memory barriers are issued). */
 hpl_status hpl_set_option(hpl_ctx *ctx, const char *name, int64_t value);
@@ -160,6 +195,22 @@ int64_t hpl_launch_count(const hpl_ctx *ctx);
  * trailing-DGEMM ms (sum of per-launch event pairs), trailing-DGEMM flop,
  * kernel launches}.  The DGEMM entries are filled only with hpl_set_timing(1). */
 hpl_status hpl_last_timing(const hpl_ctx *ctx, double *out6);
+
+/* Per-phase totals of the last hpl_factor / hpl_solve (CUDA events; the
+ * factor entries need hpl_set_timing(1)), for the roofline of every
+ * non-DGEMM kernel: out8 = {rest LASWP/RS ms, its algorithmic bytes
+ * (2 x 8 x (jb + displaced rows) x rest columns per iteration: each moved
+ * row read once and written once), rest DTRSM ms, its flop (jb^2 x rest
+ * columns per iteration), FACT ms (owner column, summed over panels), solve
+ * ms, the solve's algorithmic bytes (this rank's part of the upper triangle
+ * of U, read once), trailing-DGEMM ms}. */
+hpl_status hpl_phase_stats(const hpl_ctx *ctx, double *out8);
+
+/* Debug hook: out = {group barrier counters (world, row, column, column-tr),
+ * this rank's 4 x 32 group flag words (arrivals received per group and
+ * member), the abort word and its detail} — 4 + 128 + 2 entries (cap must
+ * be at least that).  For diagnosing a peer timeout. */
+hpl_status hpl_debug_state(const hpl_ctx *ctx, uint64_t *out, int64_t cap);
 
 /* Host-only bookkeeping of the P > 1 panel FACT of panel j on process row
  * myrow (DESIGN.md §6 "Gathered panel FACT"):

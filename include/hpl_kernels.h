@@ -22,7 +22,8 @@ extern "C" {
 
 /* a5/a6 trailing DGEMM (BASELINE north_star "A22 -= L21·U12"):
  * C (m x n, row-major ldc) -= A (m x k, col-major lda) * B (k x n, row-major ldb).
- * Runs the TMA + DMMA kernel.  cfg selects the tile configuration (0 = default). */
+ * Runs the TMA + DMMA kernel.  cfg selects the tile configuration (0: 128x64,
+ * 1: 128x128, 2: 64x64; -1 = the default, 2). */
 int hplk_dgemm_update(int64_t m, int64_t n, int64_t k,
                       const double *A, int64_t lda, const double *B, int64_t ldb,
                       double *C, int64_t ldc, int32_t cfg);
@@ -36,10 +37,17 @@ int hplk_trsm(int64_t k, int64_t n, const double *L, int64_t ldl, double *B, int
 /* a7 panel FACT: recursive right-looking LU with
  * partial pivoting, NDIV=2, leaf width nbmin, of the m x nb panel P
  * (col-major ldp), in place.  ipiv (nb entries) receives panel-relative
- * LAPACK pivots.  *info = -1, or the first column with an exact zero pivot
- * (return -2 then). */
+ * LAPACK pivots; the pivot of a column is its max |v| with ties broken
+ * towards the smallest row (a8, DESIGN reading A2).  The leaf that picks
+ * the pivots is selected like the hpl_set_option knobs of the same names:
+ * leaf_variant 0 right-looking / 1 left-looking / 2 Crout (PAPER.md
+ * l.27–34), leaf_cluster 1 = the one-cluster shared-memory leaf for panels
+ * of <= 16 x 1664 rows (0 = always the cooperative grid leaf), leaf_ctas =
+ * grid cap of the grid leaf (0 = all SMs).  *info = -1, or the first column
+ * with an exact zero pivot (return -2 then). */
 int hplk_panel_fact(int64_t m, int64_t nb, double *P, int64_t ldp, int64_t *ipiv,
-                    int32_t nbmin, int64_t *info);
+                    int32_t nbmin, int32_t leaf_variant, int32_t leaf_cluster, int32_t leaf_ctas,
+                    int64_t *info);
 
 /* a1+a3 LASWP gather/scatter ("a GPU kernel to gather the rows
  * ... and a GPU kernel to scatter"): on A (rows x cols, row-major lda), apply
@@ -59,10 +67,15 @@ int hplk_back_solve(int64_t N, int32_t NB, const double *U, int64_t ldu, const d
 int hplk_generate(uint64_t seed, int64_t N, int64_t i0, int64_t rows, int64_t j0,
                   int64_t cols, double *out);
 
-/* a8 pivot maxloc as used inside the FACT kernel: among n candidates
- * (absval[c], row[c]) return the index of the winner (max |v|, ties ->
- * smallest row) in *winner. */
-int hplk_maxloc(int64_t n, const double *absval, const int64_t *row, int64_t *winner);
+/* a11 scaled residual of the seeded system for a given x (N doubles): the
+ * kernels hpl_residual runs, on a 1 x 1 grid — A0 and b0 regenerated on the
+ * fly from the seed, never stored.  Outputs (host, may be NULL where noted):
+ * rsum[i] = sum_j A0[i][j] x[j] (N doubles, may be NULL), asum[i] = sum_j
+ * |A0[i][j]| (may be NULL), out4 = {||A0 x - b0||_inf, ||A0||_inf, ||x||_inf,
+ * ||b0||_inf} (a non-finite entry reported as +inf), *resid = the scaled
+ * residual (+inf if anything is non-finite). */
+int hplk_residual(uint64_t seed, int64_t N, const double *x, double *rsum, double *asum,
+                  double *out4, double *resid);
 
 /* Measurement hook: time `reps` launches of the trailing-update DGEMM on
  * device-resident operands (m x n x k, generator-filled), CUDA events on the

@@ -37,6 +37,7 @@ def _sig(name, res, args):
 _sig("hpl_init", ctypes.c_int, [i64, i32, i32, i32, u64, ctypes.POINTER(ctx_p)])
 _sig("hpl_init_dist", ctypes.c_int, [i64, i32, i32, i32, u64, i32, i32, vp, i32,
                                      ctypes.POINTER(ctx_p)])
+_sig("hpl_init_loopback", ctypes.c_int, [i64, i32, i32, i32, u64, i32, vp])
 _sig("hpl_get_unique_id", ctypes.c_int, [vp])
 _sig("hpl_factor", ctypes.c_int, [ctx_p])
 _sig("hpl_solve", ctypes.c_int, [ctx_p, vp])
@@ -55,6 +56,8 @@ _sig("hpl_set_timing", ctypes.c_int, [ctx_p, i32])
 _sig("hpl_set_option", ctypes.c_int, [ctx_p, ctypes.c_char_p, i64])
 _sig("hpl_launch_count", i64, [ctx_p])
 _sig("hpl_last_timing", ctypes.c_int, [ctx_p, vp])
+_sig("hpl_phase_stats", ctypes.c_int, [ctx_p, vp])
+_sig("hpl_debug_state", ctypes.c_int, [ctx_p, vp, i64])
 _sig("hpl_plan_iteration", ctypes.c_int, [i64, i32, i32, i32, i32, i32, i64, vp])
 _sig("hpl_plan_fact", ctypes.c_int, [i64, i32, i32, i32, i32, i64, i64, ctypes.c_double, vp])
 _sig("hpl_pin_host", ctypes.c_int, [vp, i64, i32])
@@ -62,23 +65,24 @@ _sig("hpl_pin_host", ctypes.c_int, [vp, i64, i32])
 # ---- include/hpl_kernels.h
 _sig("hplk_dgemm_update", ctypes.c_int, [i64, i64, i64, vp, i64, vp, i64, vp, i64, i32])
 _sig("hplk_trsm", ctypes.c_int, [i64, i64, vp, i64, vp, i64])
-_sig("hplk_panel_fact", ctypes.c_int, [i64, i64, vp, i64, vp, i32, ctypes.POINTER(i64)])
+_sig("hplk_panel_fact", ctypes.c_int, [i64, i64, vp, i64, vp, i32, i32, i32, i32,
+                                       ctypes.POINTER(i64)])
 _sig("hplk_laswp", ctypes.c_int, [i64, i64, vp, i64, i64, i64, vp, i64, i64, vp, i64])
 _sig("hplk_back_solve", ctypes.c_int, [i64, i32, vp, i64, vp, vp])
 _sig("hplk_generate", ctypes.c_int, [u64, i64, i64, i64, i64, i64, vp])
-_sig("hplk_maxloc", ctypes.c_int, [i64, vp, vp, ctypes.POINTER(i64)])
+_sig("hplk_residual", ctypes.c_int, [u64, i64, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_double)])
 _sig("hplk_dgemm_bench", ctypes.c_int, [i64, i64, i64, i32, i32, vp])
 _sig("hplk_dmma_peak", ctypes.c_int, [i32, i32, i32, vp])
 _sig("hplk_panel_bench", ctypes.c_int, [i64, i64, i32, i32, i32, vp])
 
 EXPORTED = [
-    "hpl_init", "hpl_init_dist", "hpl_get_unique_id", "hpl_factor", "hpl_solve",
+    "hpl_init", "hpl_init_dist", "hpl_init_loopback", "hpl_get_unique_id", "hpl_factor", "hpl_solve",
     "hpl_residual", "hpl_regenerate", "hpl_load_local", "hpl_local_shape", "hpl_free",
     "hpl_last_error", "hpl_singular_column", "hpl_get_ipiv", "hpl_get_local",
     "hpl_get_timeline", "hpl_get_fact_detail", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
-    "hpl_last_timing", "hpl_plan_iteration", "hpl_plan_fact", "hpl_pin_host",
+    "hpl_last_timing", "hpl_phase_stats", "hpl_debug_state", "hpl_plan_iteration", "hpl_plan_fact", "hpl_pin_host",
     "hplk_dgemm_update", "hplk_trsm", "hplk_panel_fact", "hplk_laswp", "hplk_back_solve",
-    "hplk_generate", "hplk_maxloc", "hplk_dgemm_bench", "hplk_dmma_peak", "hplk_panel_bench",
+    "hplk_generate", "hplk_residual", "hplk_dgemm_bench", "hplk_dmma_peak", "hplk_panel_bench",
 ]
 
 

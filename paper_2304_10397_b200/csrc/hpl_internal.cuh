@@ -1,18 +1,119 @@
 // hpl_internal.cuh — shared declarations of libhpl.so's kernels and launchers.
 // Product code only; nothing here is shared with oracle/ (see DESIGN.md).
+//
+// Every knob lives in the caller's context (FactWork, the dgemm cfg
+// argument): there is no process-wide mutable state, so several contexts can
+// drive the library from several host threads at once (the single-device
+// P x Q loopback).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <atomic>
+#include <algorithm>
 
 namespace hpl {
 
-// Number of this library's kernel launches (reported as gpu_launches).
-extern std::atomic<int64_t> g_launches;
-inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Number of this library's kernel launches issued by the calling host thread
+// (each rank of a loopback grid runs on its own thread; reported as
+// gpu_launches).
+extern thread_local int64_t t_launches;
+inline void count_launch(int64_t n = 1) { t_launches += n; }
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- bounded peer waits
+// Every spin on a flag another rank (or another CTA) writes is bounded: it
+// gives up when this context's abort word is set, or sets it (with a site
+// code) once timeout_ns of %globaltimer have passed.  A dead or absent peer
+// therefore ends hpl_factor / hpl_solve / hpl_residual with HPL_ERR_PEER
+// instead of spinning forever (a deadlock surfaces as
+// an error).  After an abort every later wait of the context returns at
+// once, the kernels finish on garbage and the context must be freed.
+struct SpinCtl {
+    unsigned long long *abort;      // device word: 0 = running, else the first failing site
+    unsigned long long timeout_ns;
+};
+enum SpinSite : unsigned {
+    SITE_GRID_BARRIER = 1, SITE_DIST_PEER = 2, SITE_DIST_WIN = 3, SITE_RS_BARRIER = 4,
+    SITE_FLAG = 5, SITE_GROUP_BARRIER = 6
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ bool spin_aborted(const SpinCtl &sc)
+{
+    return *reinterpret_cast<volatile const unsigned long long *>(sc.abort) != 0ull;
+}
+// Record the first abandoned wait: abort[0] = site code (low 4 bits: the
+// SpinSite; above them a site-specific detail such as the group and member
+// waited for), abort[1] = expected value << 32 | value seen (low 32 bits).
+__device__ __forceinline__ void spin_record(const SpinCtl &sc, unsigned long long code,
+                                            unsigned long long want, unsigned long long seen)
+{
+    if (atomicCAS(sc.abort, 0ull, code) == 0ull)
+        sc.abort[1] = (want << 32) | (seen & 0xffffffffull);
+}
+// Wait until *p >= v (system-scope acquire).  false: abandoned (abort/timeout).
+__device__ __forceinline__ bool spin_geq_sys(const unsigned long long *p, unsigned long long v,
+                                             const SpinCtl &sc, unsigned long long site)
+{
+    if (ld_acquire_sys(p) >= v) return true;
+    const unsigned long long t0 = gtimer();
+    for (unsigned n = 1;; ++n) {
+        if (ld_acquire_sys(p) >= v) return true;
+        if ((n & 15u) == 0) {
+            if (spin_aborted(sc)) return false;
+            if (gtimer() - t0 > sc.timeout_ns) {
+                spin_record(sc, site, v, ld_acquire_sys(p));
+                return false;
+            }
+        }
+        __nanosleep(64);
+    }
+}
+// Same at GPU scope (flags written by other CTAs of this GPU).
+__device__ __forceinline__ bool spin_geq_gpu(const unsigned long long *p, unsigned long long v,
+                                             const SpinCtl &sc, unsigned long long site)
+{
+    if (ld_acquire_gpu(p) >= v) return true;
+    const unsigned long long t0 = gtimer();
+    for (unsigned n = 1;; ++n) {
+        if (ld_acquire_gpu(p) >= v) return true;
+        if ((n & 63u) == 0) {
+            if (spin_aborted(sc)) return false;
+            if (gtimer() - t0 > sc.timeout_ns) {
+                spin_record(sc, site, v, ld_acquire_gpu(p));
+                return false;
+            }
+        }
+    }
+}
+#endif
 
 // ---------------------------------------------------------------- generator
 // Fill local block: rows [0, lrows) x cols [0, lcols) of the row-major local
@@ -39,20 +140,17 @@ enum GemmMode { GEMM_UPDATE = 0, GEMM_ASSIGN = 1 };
 // a_lower: A is lower triangular (A[i][p] = 0 for p > i): k-chunks above the
 // diagonal of each m-tile are skipped.  A and B must be 16-byte aligned with
 // even lda/ldb (TMA); C may be anywhere.  C2 (ASSIGN only, 16B aligned, even
-// ldc2): the epilogue stores the result there as well.  slot (0..2) selects
-// the param-space offset of the kernel's tensor maps: launches that may run
-// concurrently must use different slots (see kernels_gemm.cu ParamPad).
-enum GemmSlot { SLOT_TRAIL = 0, SLOT_LOOKAHEAD = 1, SLOT_FACT = 2 };
+// ldc2): the epilogue stores the result there as well.  cfg: tile config
+// (0: 128x64, 1: 128x128, 2: 64x64 = DGEMM_DEFAULT_CFG; -1 = default).
+// slot selects the param-space offset of the kernel's tensor maps: launches
+// that may run concurrently must use different slots (see kernels_gemm.cu
+// ParamPad); the driver picks the slot from the stream.
+constexpr int DGEMM_DEFAULT_CFG = 2;
+enum GemmSlot { SLOT_TRAIL = 0, SLOT_LOOKAHEAD = 1, SLOT_FACT = 2, SLOT_RS = 3 };
 cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n, int64_t k,
                   const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                   int64_t ldc, int cfg = -1, double *C2 = nullptr, int64_t ldc2 = 0,
                   int slot = SLOT_TRAIL);
-void dgemm_set_default_cfg(int cfg);
-// Tiles per CTA for large DGEMM grids (1 = one tile per CTA).
-void dgemm_set_tiles_per_cta(int t);
-// UPDATE epilogue via red.global.add.f64 (no C load round trip); 0 = load/sub/store.
-void dgemm_set_red_epilogue(int on);
-int dgemm_get_default_cfg();
 
 // ---------------------------------------------------------------- TRSM helpers
 // In-place B (k x ncols, col-major ldb) <- L^{-1} B, L unit lower (col-major ldl),
@@ -62,18 +160,31 @@ cudaError_t trsm_cols(cudaStream_t st, int64_t k, int64_t ncols, const double *L
                       double *B, int64_t ldb, bool identity_init);
 
 // ---------------------------------------------------------------- panel FACT
+// Per-context FACT workspace and leaf policy (formerly process-wide knobs).
 struct FactWork {
     double *cand;        // candidate records (2 parity buffers)
-    unsigned *bar;       // grid barrier words (count, generation)
+    unsigned *bar;       // grid barrier words (count, generation) + winner flag
     int64_t *info;       // first singular global column; all-ones (== -1) if none
     double *win;         // P > 1: winning pivot record (global row + full panel row)
     double *tsnap;       // P > 1: snapshot of the replicated top row kc
-    int max_ctas;
+    unsigned long long *abort;   // SpinCtl abort word of the owning context
+    unsigned long long timeout_ns;
+    int max_ctas;        // hard cap of every leaf grid (loopback: SMs / ranks)
+    int num_sms;
+    // leaf policy
+    int leaf_max_ctas = 0;       // 0 = all SMs (up to max_ctas)
+    int leaf_rows_per_cta = 512;
+    int leaf_warp_ctas = 0;      // > 0: one-warp CTAs (co-resident with the DGEMM), at most this many
+    int leaf_variant = 0;        // 0 right-looking, 1 left-looking, 2 Crout
+    int leaf_cluster = 1;        // one-cluster shared-memory leaf for small panels
+    int gemm_cfg = -1;           // DGEMM tile config of the recursion's updates
+    int plain_launch = 0;        // loopback: leaf grids by a plain launch (kernels_fact.cu launch_grid)
+    SpinCtl spin() const { return SpinCtl{abort, timeout_ns}; }
 };
 
 // P > 1 panel FACT: the P processes of the panel's process column exchange
 // pivot candidates (value, global row, full panel row) through peer memory
-// (CUDA IPC over NVLink) inside the leaf kernel.
+// (CUDA IPC over NVLink, or plain pointers in the loopback) inside the leaf.
 constexpr int MAX_P = 8;
 struct DistExchange {
     double *rec[MAX_P];                 // record area on each peer (index = process row)
@@ -97,10 +208,7 @@ struct DistFact {
 cudaError_t fact_work_alloc(FactWork *w);
 // Leaf grid size: min(max_ctas (0 = #SMs), ceil(rows / rows_per_cta)).  Fewer
 // CTAs leave more of each SM to the concurrent trailing DGEMM.
-void fact_set_leaf_ctas(int max_ctas, int rows_per_cta);
-// > 0: leaves run as one-warp CTAs (at most this many) that fit next to the
-// trailing DGEMM's CTAs; 0: the multi-warp leaf with fact_set_leaf_ctas' grid
-void fact_set_leaf_warp_ctas(int ctas);
+void fact_set_leaf_ctas(FactWork *w, int max_ctas, int rows_per_cta);
 // Gathered panel FACT (P > 1, small panels): every process of the column
 // builds the combined panel (row c = global row j0 + c) from the packed
 // panels of all P processes (peer memory), factors it with the one-GPU FACT
@@ -117,17 +225,6 @@ cudaError_t fact_gather(cudaStream_t st, int64_t rows, int64_t jb, int64_t j0, i
 cudaError_t fact_extract(cudaStream_t st, int64_t mine, int64_t jb, int64_t j0, int NB, int P,
                          int myrow, int64_t lrL0, const double *Cp, int64_t ldc, double *Pn,
                          int64_t ldp);
-// Leaf variant of the P = 1 panel FACT: 0 right-looking
-// (default), 1 left-looking, 2 Crout — bitwise-equal results.  P > 1 panels
-// always use the right-looking distributed leaf.
-void fact_set_leaf_variant(int v);
-// Small panels (<= 16 x 1664 rows) use the one-cluster shared-memory leaf
-// (DSMEM candidates, hardware cluster barrier); 0 = always the grid leaf.
-void fact_set_leaf_cluster(int on);
-int fact_get_leaf_variant();
-// Pivot winner among n candidates (max |v|, ties -> smallest row), as the FACT reduces.
-cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,
-                       int64_t *winner);
 void fact_work_free(FactWork *w);
 // Recursive right-looking panel LU (NDIV=2, leaf nbmin) of P (m x nb col-major ldp).
 // ipiv receives panel-relative pivots (device, int64).  Uses scratch for the
@@ -141,16 +238,17 @@ cudaError_t panel_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_
 // From panel-relative pivots (jb entries; positions r0+k <-> r0+ipiv_rel[k])
 // build: src[k] (row whose content ends in row r0+k, k<jb), and ndisp
 // displaced (dst, src) row pairs (dst >= r0+jb).  Also writes global pivots
-// gpiv[k] = ipiv_rel[k] + goff.  All device arrays.
+// gpiv[k] = ipiv_rel[k] + goff.  Rows are < nrows; a pivot outside
+// [r0+k, nrows) (only after an aborted FACT) is taken as no interchange.
+// All device arrays.
 cudaError_t pivot_plan(cudaStream_t st, int64_t jb, int64_t r0, const int64_t *ipiv_rel,
-                       int64_t goff, int64_t *gpiv, int64_t *src, int64_t *disp,
+                       int64_t goff, int64_t nrows, int64_t *gpiv, int64_t *src, int64_t *disp,
                        int *ndisp);
 // Gather U[k][c] = A[src[k]][c0+c] and scatter A[disp_dst][c] = A[disp_src][c]
 // for columns [c0, c1) of the row-major A.
 cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src,
-                                 const int64_t *disp, const int *ndisp, int64_t max_disp,
-                                 double *A, int64_t lda, int64_t c0, int64_t c1, double *U,
-                                 int64_t ldu);
+                                 const int64_t *disp, const int *ndisp, double *A, int64_t lda,
+                                 int64_t c0, int64_t c1, double *U, int64_t ldu);
 
 // P > 1 row swaps (RS): pack the rows of U this process row owns (zeros
 // elsewhere; summed over the process column by the caller), and scatter the
@@ -174,7 +272,8 @@ struct RsPeers {
 };
 // Flag barrier over the process column at `slot` (monotonic value): one
 // one-warp kernel; every later kernel on st sees the peers' earlier writes.
-cudaError_t rs_barrier(cudaStream_t st, const RsPeers &pr, int slot, unsigned long long value);
+cudaError_t rs_barrier(cudaStream_t st, const RsPeers &pr, int slot, unsigned long long value,
+                       const SpinCtl &sc);
 // Phase 1 of the peer-memory RS for local columns [c0, c1): U[k] = global row
 // src[k] read from its owner; W[s - j0] = original block row s (from the
 // owner of block row j0) for every displaced pair (d, s) whose d this process owns.
@@ -191,7 +290,39 @@ struct FlagOp {
     int nsig, nwait;
     unsigned long long sv, wv;
 };
-cudaError_t flag_op(cudaStream_t st, const FlagOp &op);
+cudaError_t flag_op(cudaStream_t st, const FlagOp &op, const SpinCtl &sc);
+
+// ---------------------------------------------------------------- peer collectives
+// Collectives over a group of ranks (world / process row / process column)
+// through peer memory, for the exchanges that are not the hot-path RS /
+// LBCAST / pivot search: the replicated top block of the P > 1 FACT, the
+// back-solve reductions and broadcasts, the residual norms, the singular
+// column.  Each rank owns a CommBlock (device memory, IPC-mapped by its peers
+// or a plain pointer in the loopback); a collective stages this rank's data
+// in its own block, passes a flag barrier, reads every member's stage in a
+// fixed member order (the same result bits on every rank), and passes a
+// second barrier before the stage is reused.
+constexpr int MAX_GROUP = 32;
+constexpr int N_GROUPS = 4;                       // world, row, column, column (trailing stream)
+constexpr int64_t STAGE_DOUBLES = int64_t(1) << 19;   // 4 MB per group
+struct CommBlock {
+    unsigned long long flag[N_GROUPS][MAX_GROUP];   // barrier arrival words [group][member]
+    double stage[N_GROUPS][STAGE_DOUBLES];
+};
+struct GroupDev {
+    CommBlock *blk[MAX_GROUP];    // member m's block (own block at index me)
+    int size, me, gid;
+};
+enum CollOp { COLL_SUM = 0, COLL_MAX = 1, COLL_MIN_U64 = 2 };
+cudaError_t group_barrier(cudaStream_t st, const GroupDev &g, unsigned long long value,
+                          const SpinCtl &sc);
+// Device-to-device 2D copy (rows x width bytes) and an 8-byte store, done by
+// SMs instead of the copy engine: the loopback's copies (hpl_comm.cu d2d).
+cudaError_t copy2d_sm(cudaStream_t st, void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                      int64_t width, int64_t rows);
+cudaError_t fill_u64(cudaStream_t st, unsigned long long *p, unsigned long long v);
+// out[i] = op over members m = 0..size-1 (in order) of member m's stage[gid][i].
+cudaError_t group_reduce(cudaStream_t st, const GroupDev &g, int op, int64_t n, void *out);
 
 // ---------------------------------------------------------------- solve / residual
 // Single-matrix back solve (y = column N of U's rows): hplk_back_solve.
@@ -209,13 +340,24 @@ cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
                     const double *partial, int S, double *xb);
 // Residual of the seeded system: per-rank partial sums (local rows x local
 // columns), then (after the caller's all-reduce over the process row) the
-// norms into out4 = {rinf, anorm, xnorm, bnorm} (max over local rows).
+// norms into out4 = {rinf, anorm, xnorm, bnorm} (max over local rows; a
+// non-finite value anywhere makes the corresponding entry +inf).
 cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
                              int64_t mloc, int Q, int mycol, int64_t lcols, const double *x,
                              double *r, double *a);
 cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
                               int64_t mloc, const double *r, const double *a, const double *x,
                               double *out4);
+
+// HPL's scaled residual from out4 = {||r||, ||A0||, ||x||, ||b0||} (SPEC.md
+// l.383-391, eps = 2^-53, reading A4); a non-finite part gives +inf.
+inline double scaled_residual(const double *h, int64_t N)
+{
+    for (int k = 0; k < 4; ++k)
+        if (!(h[k] - h[k] == 0.0)) return __builtin_inf();   // inf or NaN
+    const double r = h[0] / (0x1p-53 * (h[1] * h[2] + h[3]) * (double)N);
+    return r == r ? r : __builtin_inf();
+}
 
 // FP64 tensor-pipe ceiling: register-resident DMMA chain on every SM.
 cudaError_t dmma_peak(int iters, int blocks_per_sm, int warps, double *ms, double *flop);

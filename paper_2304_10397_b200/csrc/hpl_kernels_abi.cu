@@ -71,9 +71,10 @@ int hplk_trsm(int64_t k, int64_t n, const double *L, int64_t ldl, double *B, int
 }
 
 int hplk_panel_fact(int64_t m, int64_t nb, double *P, int64_t ldp, int64_t *ipiv, int32_t nbmin,
-                    int64_t *info)
+                    int32_t leaf_variant, int32_t leaf_cluster, int32_t leaf_ctas, int64_t *info)
 {
     if (m < nb || nb < 1 || ldp < m || nbmin < 1 || nbmin > 16) return -1;
+    if (leaf_variant < 0 || leaf_variant > 2 || leaf_ctas < 0) return -1;
     const int64_t dlp = round_up(m, 16);
     Dev dP, dI, dS;
     FactWork fw{};
@@ -83,6 +84,9 @@ int hplk_panel_fact(int64_t m, int64_t nb, double *P, int64_t ldp, int64_t *ipiv
     KT(cudaMemset(dP.p, 0, sizeof(double) * dlp * nb));
     KT(cudaMemcpy2D(dP.p, dlp * 8, P, ldp * 8, m * 8, nb, cudaMemcpyHostToDevice));
     KT(fact_work_alloc(&fw));
+    fw.leaf_variant = leaf_variant;
+    fw.leaf_cluster = leaf_cluster != 0;
+    fact_set_leaf_ctas(&fw, leaf_ctas, 0);
     cudaError_t e = panel_fact(0, m, nb, dP.as<double>(), dlp, dI.as<int64_t>(), nbmin, &fw,
                                dS.as<double>(), 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -120,9 +124,9 @@ int hplk_laswp(int64_t rows, int64_t cols, double *A, int64_t lda, int64_t j0, i
     KT(dN.alloc(sizeof(int)));
     KT(cudaMemcpy2D(dA.p, dla * 8, A, lda * 8, cols * 8, rows, cudaMemcpyHostToDevice));
     KT(cudaMemcpy(dRel.p, rel.data(), sizeof(int64_t) * jb, cudaMemcpyHostToDevice));
-    KT(pivot_plan(0, jb, j0, dRel.as<int64_t>(), j0, dG.as<int64_t>(), dSrc.as<int64_t>(),
+    KT(pivot_plan(0, jb, j0, dRel.as<int64_t>(), j0, rows, dG.as<int64_t>(), dSrc.as<int64_t>(),
                   dDisp.as<int64_t>(), dN.as<int>()));
-    KT(laswp_gather_scatter(0, jb, dSrc.as<int64_t>(), dDisp.as<int64_t>(), dN.as<int>(), jb,
+    KT(laswp_gather_scatter(0, jb, dSrc.as<int64_t>(), dDisp.as<int64_t>(), dN.as<int>(),
                             dA.as<double>(), dla, c0, c1, dU.as<double>(), dlu));
     KT(cudaDeviceSynchronize());
     KT(cudaMemcpy2D(A, lda * 8, dA.p, dla * 8, cols * 8, rows, cudaMemcpyDeviceToHost));
@@ -164,29 +168,32 @@ int hplk_generate(uint64_t seed, int64_t N, int64_t i0, int64_t rows, int64_t j0
     return 0;
 }
 
-int hplk_maxloc(int64_t n, const double *absval, const int64_t *row, int64_t *winner)
+int hplk_residual(uint64_t seed, int64_t N, const double *x, double *rsum, double *asum,
+                  double *out4, double *resid)
 {
-    if (n < 1 || !absval || !row || !winner) return -1;
-    Dev dv, dr, dw;
-    KT(dv.alloc(sizeof(double) * n));
-    KT(dr.alloc(sizeof(int64_t) * n));
-    KT(dw.alloc(sizeof(int64_t)));
-    KT(cudaMemcpy(dv.p, absval, sizeof(double) * n, cudaMemcpyHostToDevice));
-    KT(cudaMemcpy(dr.p, row, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
-    KT(maxloc_dev(0, (int)n, dv.as<double>(), dr.as<int64_t>(), dw.as<int64_t>()));
+    if (N < 1 || !x || !out4 || !resid) return -1;
+    Dev dx, dr, da, d4;
+    KT(dx.alloc(sizeof(double) * N));
+    KT(dr.alloc(sizeof(double) * N));
+    KT(da.alloc(sizeof(double) * N));
+    KT(d4.alloc(sizeof(double) * 4));
+    KT(cudaMemcpy(dx.p, x, sizeof(double) * N, cudaMemcpyHostToDevice));
+    // the kernels hpl_residual runs on a 1 x 1 grid (block-cyclic map = identity)
+    KT(residual_partial(0, seed, N, 1, 1, 0, N, 1, 0, N, dx.as<double>(), dr.as<double>(),
+                        da.as<double>()));
+    KT(residual_finalize(0, seed, N, 1, 1, 0, N, dr.as<double>(), da.as<double>(),
+                         dx.as<double>(), d4.as<double>()));
     KT(cudaDeviceSynchronize());
-    KT(cudaMemcpy(winner, dw.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (rsum) KT(cudaMemcpy(rsum, dr.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    if (asum) KT(cudaMemcpy(asum, da.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    KT(cudaMemcpy(out4, d4.p, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+    *resid = scaled_residual(out4, N);
     return 0;
 }
 
 int hplk_dgemm_bench(int64_t m, int64_t n, int64_t k, int32_t cfg, int32_t reps, double *ms_out)
 {
-    if (m < 1 || n < 1 || k < 1 || reps < 1 || !ms_out) return -1;
-    if (cfg >= 0) {     // cfg = 1000 * red_epilogue + 100 * tiles_per_cta + tile config
-        dgemm_set_red_epilogue(cfg / 1000);
-        dgemm_set_tiles_per_cta(std::max(1, (cfg % 1000) / 100));
-        cfg %= 100;
-    }
+    if (m < 1 || n < 1 || k < 1 || reps < 1 || !ms_out || cfg < -1 || cfg > 2) return -1;
     const int64_t lda = round_up(m, 16), ldb = round_up(n, 16), ldc = ldb;
     Dev dA, dB, dC;
     KT(dA.alloc(sizeof(double) * lda * k));
@@ -226,7 +233,7 @@ int hplk_panel_bench(int64_t m, int64_t nb, int32_t nbmin, int32_t leaf_ctas, in
     KT(dI.alloc(sizeof(int64_t) * nb));
     KT(dS.alloc(sizeof(double) * round_up(nb, 16) * nb));
     KT(fact_work_alloc(&fw));
-    fact_set_leaf_ctas(leaf_ctas, 512);
+    fact_set_leaf_ctas(&fw, leaf_ctas, 512);
     cudaEvent_t e0, e1;
     KT(cudaEventCreate(&e0));
     KT(cudaEventCreate(&e1));
@@ -245,7 +252,6 @@ int hplk_panel_bench(int64_t m, int64_t nb, int32_t nbmin, int32_t leaf_ctas, in
         if (r >= 0) ms_out[r] = t;
     }
     KT(cudaMemcpy(&inf, fw.info, sizeof inf, cudaMemcpyDeviceToHost));
-    fact_set_leaf_ctas(0, 512);
     fact_work_free(&fw);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -15,6 +15,7 @@
 #include "hpl_internal.cuh"
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <mutex>
 
 namespace hpl {
 
@@ -25,7 +26,10 @@ constexpr int REC = 2 + LEAF_MAX;      // doubles per candidate record
 constexpr int FACT_THREADS = 256;
 constexpr int MAX_CTAS = 1024;
 
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks)
+// Software grid barrier of the cooperative leaf (co-residency guaranteed by
+// the cooperative launch).  Bounded like every other spin (SpinCtl): after
+// an abort the CTAs leave it at once.
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks, const SpinCtl &sc)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -38,7 +42,15 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks)
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*gen == g0) {
+            const unsigned long long t0 = gtimer();
+            for (unsigned n = 1; *gen == g0; ++n) {
+                if ((n & 63u) == 0) {
+                    if (spin_aborted(sc)) break;
+                    if (gtimer() - t0 > sc.timeout_ns) {
+                        spin_record(sc, SITE_GRID_BARRIER, g0 + 1, *gen);
+                        break;
+                    }
+                }
             }
         }
         __threadfence();
@@ -101,7 +113,7 @@ __device__ __forceinline__ double leaf_row_update(double *P, int64_t ldp, int k0
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1)
 leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, double *cand,
-                 unsigned *bar, unsigned long long *info, long long goff)
+                 unsigned *bar, unsigned long long *info, long long goff, SpinCtl sc)
 {
     const unsigned G = gridDim.x;
     const int nrows = m - k0;
@@ -144,7 +156,7 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
                 rec[(size_t)G * REC + 2 + threadIdx.x] = P[(int64_t)(k0 + threadIdx.x) * ldp + kc];
         }
         __threadfence();
-        grid_barrier(bar, G);
+        grid_barrier(bar, G, sc);
 
         // ---- 2. every CTA reduces all candidates (deterministic)
         bv = -1.0;
@@ -179,6 +191,9 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
                 const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
                 if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
             }
+            // (bc < 0 only if no CTA reported a candidate: after an abandoned
+            // barrier; read a valid slot, the pivot is discarded downstream)
+            if (bc < 0) bc = 0;
             if (threadIdx.x == 0) {
                 s_p = br;
                 s_piv = __ldcg(rec + (size_t)bc * REC + 2 + kk);
@@ -230,7 +245,7 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
 template <int NT, bool CROUT>
 __global__ void __launch_bounds__(NT, 1)
 leaf_fact_ll_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, double *cand,
-                    unsigned *bar, unsigned long long *info, long long goff)
+                    unsigned *bar, unsigned long long *info, long long goff, SpinCtl sc)
 {
     const unsigned G = gridDim.x;
     const int nrows = m - k0;
@@ -278,7 +293,7 @@ leaf_fact_ll_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv,
                 rec[(size_t)G * REC + 2 + threadIdx.x] = P[(int64_t)(k0 + threadIdx.x) * ldp + kc];
         }
         __threadfence();
-        grid_barrier(bar, G);
+        grid_barrier(bar, G, sc);
 
         // ---- 2. every CTA reduces all candidates (deterministic)
         bv = -1.0;
@@ -312,6 +327,9 @@ leaf_fact_ll_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv,
                 const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
                 if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
             }
+            // (bc < 0 only if no CTA reported a candidate: after an abandoned
+            // barrier; read a valid slot, the pivot is discarded downstream)
+            if (bc < 0) bc = 0;
             if (threadIdx.x == 0) {
                 s_p = br;
                 s_piv = __ldcg(rec + (size_t)bc * REC + 2 + kk);
@@ -381,7 +399,7 @@ leaf_fact_ll_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv,
 // swaps into "row r receives the old content of row s" moves (as pivot_plan
 // does for the trailing matrix); each thread then moves its column's rows
 // with all loads issued before the stores.
-__global__ void panel_laswp_kernel(int nb, int64_t ldp, double *P, int k0, int w,
+__global__ void panel_laswp_kernel(int m, int nb, int64_t ldp, double *P, int k0, int w,
                                    const int64_t *ipiv)
 {
     __shared__ long long s_dst[2 * LEAF_MAX], s_src[2 * LEAF_MAX];
@@ -392,7 +410,8 @@ __global__ void panel_laswp_kernel(int nb, int64_t ldp, double *P, int k0, int w
         for (int t = 0; t < w; ++t) topc[t] = k0 + t;
         for (int t = 0; t < w; ++t) {
             const long long pp = ipiv[k0 + t];
-            if (pp == k0 + t) continue;
+            // (a pivot outside [k0+t, m) only follows an aborted leaf: skipped)
+            if (pp == k0 + t || pp < k0 + t || pp >= m) continue;
             if (pp < k0 + w) {
                 const long long tmp = topc[t];
                 topc[t] = topc[pp - k0];
@@ -428,27 +447,6 @@ __global__ void panel_laswp_kernel(int nb, int64_t ldp, double *P, int k0, int w
 }
 
 // ---------------------------------------------------------------- P > 1 leaf
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v)
-{
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v)
-{
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 // Leaf of the distributed panel: as leaf_fact_kernel, but the candidate search
 // spans the process column.  Per column: local candidates -> grid barrier ->
 // CTA 0 publishes (|v|, global row, the full panel row) into every peer's
@@ -462,7 +460,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1)
 leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ipiv, double *cand,
                       double *win, double *tsnap, unsigned long long *winflag, unsigned *bar,
                       unsigned long long *info, DistPanel dp, DistExchange ex,
-                      unsigned long long seq0)
+                      unsigned long long seq0, SpinCtl sc)
 {
     const unsigned G = gridDim.x;
     const int chunk = (m + (int)G - 1) / (int)G;
@@ -512,7 +510,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         }
         int brr;
         __threadfence();
-        grid_barrier(bar, G);
+        grid_barrier(bar, G, sc);
 
         // ---- 3. CTA 0: process-column exchange.  The other CTAs wait on the
         // local "winner ready" flag instead of a second grid barrier.
@@ -551,9 +549,12 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
             // system-scope release of the flag (cumulativity)
             __syncthreads();
             if (threadIdx.x < ex.P) {
+                // flags of one parity slot only grow (seq advances by 2 between
+                // its uses) and no peer can pass column seq before this one
+                // published it, so ">= seq" is "== seq"
                 st_release_sys(ex.flag[threadIdx.x] + (size_t)par * ex.P + ex.myrow, seq);
-                while (ld_acquire_sys(ex.my_flag + (size_t)par * ex.P + threadIdx.x) != seq) {
-                }
+                spin_geq_sys(ex.my_flag + (size_t)par * ex.P + threadIdx.x, seq, sc,
+                             SITE_DIST_PEER | (unsigned long long)threadIdx.x << 8);
             }
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -565,7 +566,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
                     const long long g = __double_as_longlong(__ldcv(r + 1));
                     if (g != LLONG_MAX && better(v, g, bv, bg)) { bv = v; bg = g; wslot = p; }
                 }
-                s_r[0] = wslot;
+                s_r[0] = wslot < 0 ? ex.myrow : wslot;   // (< 0 only after an abort)
                 s_win = bg;
                 win[0] = __longlong_as_double(bg);
             }
@@ -583,9 +584,7 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
                 st_release_gpu(winflag, seq);
             }
         } else {
-            if (threadIdx.x == 0)
-                while (ld_acquire_gpu(winflag) != seq) {
-                }
+            if (threadIdx.x == 0) spin_geq_gpu(winflag, seq, sc, SITE_DIST_WIN);
             __syncthreads();
             if (threadIdx.x == 0) s_win = __double_as_longlong(__ldcg(win));
             for (int c = threadIdx.x; c < jbp; c += NT) {
@@ -761,7 +760,6 @@ leaf_fact_cluster_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *
     cl.sync();   // no CTA leaves while a peer could still address its shared memory
 }
 
-int g_leaf_cluster = 1;         // cluster leaf for panels of <= CL_SIZE * CL_ROWS rows
 
 // ---------------------------------------------------------------- gathered FACT (P > 1 tail)
 // Combined panel Cp (column-major, ldc): row c = global row j0 + c.  Rows
@@ -804,116 +802,130 @@ __global__ void fact_extract_kernel(int mine, int jb, int cols, long long j0, in
     for (int k = blockIdx.y; k < cols; k += gridDim.y) Pn[(long long)k * ldp + r] = Cp[(long long)k * ldc + c];
 }
 
-int g_num_sms = 0;
-int g_leaf_max_ctas = 0;        // 0 = all SMs
-int g_leaf_rows_per_cta = 512;
-int g_leaf_warp_ctas = 0;       // > 0: one-warp CTAs (co-resident with the DGEMM), at most this many
-int g_leaf_variant = 0;         // 0 right-looking, 1 left-looking, 2 Crout (leaf_fact_ll_kernel)
 constexpr int WARP_LEAF_MIN_ROWS = 128;
 
-// grid of the next leaf launch: {CTAs, threads per CTA}
-void leaf_grid(int64_t rows, int max_ctas, int *G, int *NT)
+// The leaf's CTAs meet at a software grid barrier, so they must be resident
+// together: a cooperative launch guarantees that on a GPU with one rank.  In
+// the single-device loopback the ranks' leaves also wait on each other, and
+// there cooperative launches were measured to stall the device's dispatch
+// for seconds now and then (tests/test_loopback.py); the
+// loopback caps every leaf grid at SMs / (P*Q) CTAs, so a plain launch is
+// co-resident as soon as the (non-waiting) work around it drains.
+cudaError_t launch_grid(const FactWork *wk, const void *fn, int G, int NT, void **args,
+                        cudaStream_t st)
 {
-    if (g_leaf_warp_ctas > 0) {
+    if (wk->plain_launch) return cudaLaunchKernel(fn, dim3(G), dim3(NT), args, 0, st);
+    return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), args, 0, st);
+}
+
+void ensure_sms(FactWork *wk)
+{
+    if (wk->num_sms <= 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&wk->num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (wk->num_sms <= 0) wk->num_sms = 148;
+    }
+}
+
+// grid of the next leaf launch: {CTAs, threads per CTA} from the context's policy
+void leaf_grid(const FactWork *wk, int64_t rows, int *G, int *NT)
+{
+    if (wk->leaf_warp_ctas > 0) {
         *NT = 32;
         *G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, WARP_LEAF_MIN_ROWS)),
-                                    std::min(g_leaf_warp_ctas, max_ctas));
+                                    std::min(wk->leaf_warp_ctas, wk->max_ctas));
         return;
     }
-    const int gmax = g_leaf_max_ctas > 0 ? std::min(g_leaf_max_ctas, g_num_sms) : g_num_sms;
+    const int gmax = wk->leaf_max_ctas > 0 ? std::min(wk->leaf_max_ctas, wk->num_sms) : wk->num_sms;
     *NT = FACT_THREADS;
-    *G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, g_leaf_rows_per_cta)), gmax);
-    *G = std::min(*G, max_ctas);
+    *G = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(rows, wk->leaf_rows_per_cta)), gmax);
+    *G = std::min(*G, wk->max_ctas);
 }
 
 cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
                         int64_t *ipiv, FactWork *wk, long long goff)
 {
-    if (!g_num_sms) {
-        int dev;
-        HPL_CUDA_TRY(cudaGetDevice(&dev));
-        HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    if (g_leaf_cluster && g_leaf_variant == 0 && g_leaf_warp_ctas == 0 &&
+    ensure_sms(wk);
+    unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
+    if (wk->leaf_cluster && wk->leaf_variant == 0 && wk->leaf_warp_ctas == 0 &&
         m - k0 <= (int64_t)CL_SIZE * CL_ROWS && w <= LEAF_MAX && w > 0 && m - k0 > 0) {
         const int chunk = (int)cdiv(m - k0, CL_SIZE);
         const size_t smem = sizeof(double) * (size_t)chunk * w;
-        static bool attr = false;
-        if (!attr) {
-            HPL_CUDA_TRY(cudaFuncSetAttribute(leaf_fact_cluster_kernel,
-                                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            HPL_CUDA_TRY(cudaFuncSetAttribute(leaf_fact_cluster_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)(sizeof(double) * CL_ROWS * LEAF_MAX)));
-            attr = true;
+        static std::once_flag once;
+        static cudaError_t attr_err = cudaSuccess;
+        std::call_once(once, [] {
+            attr_err = cudaFuncSetAttribute(leaf_fact_cluster_kernel,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (attr_err == cudaSuccess)
+                attr_err = cudaFuncSetAttribute(leaf_fact_cluster_kernel,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(sizeof(double) * CL_ROWS * LEAF_MAX));
+        });
+        cudaError_t e = attr_err;
+        if (e == cudaSuccess) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(CL_SIZE);
+            cfg.blockDim = dim3(CL_THREADS);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CL_SIZE;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, leaf_fact_cluster_kernel, (int)m, ldp, P, k0, w, ipiv,
+                                   info, goff, chunk);
         }
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(CL_SIZE);
-        cfg.blockDim = dim3(CL_THREADS);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = CL_SIZE;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, leaf_fact_cluster_kernel, (int)m, ldp, P,
-                                                 k0, w, ipiv,
-                                                 reinterpret_cast<unsigned long long *>(wk->info),
-                                                 goff, chunk);
         if (e == cudaSuccess) {
             count_launch();
             return cudaSuccess;
         }
-        // a device that cannot place a 16-CTA cluster: the grid leaf from now on
+        // a device that cannot place a 16-CTA cluster: this context's grid leaf from now on
         cudaGetLastError();
-        g_leaf_cluster = 0;
+        wk->leaf_cluster = 0;
     }
     int G, NT;
-    leaf_grid(m - k0, wk->max_ctas, &G, &NT);
+    leaf_grid(wk, m - k0, &G, &NT);
     int m_i = (int)m;
     int64_t ldp_ = ldp;
     int k0_ = k0, w_ = w;
-    unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
-    void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->bar, &info, &goff};
+    SpinCtl sc = wk->spin();
+    void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->bar, &info, &goff, &sc};
     const void *fn = NT == 32 ? (const void *)leaf_fact_kernel<32>
                               : (const void *)leaf_fact_kernel<FACT_THREADS>;
-    if (g_leaf_variant == 1)
+    if (wk->leaf_variant == 1)
         fn = NT == 32 ? (const void *)leaf_fact_ll_kernel<32, false>
                       : (const void *)leaf_fact_ll_kernel<FACT_THREADS, false>;
-    else if (g_leaf_variant == 2)
+    else if (wk->leaf_variant == 2)
         fn = NT == 32 ? (const void *)leaf_fact_ll_kernel<32, true>
                       : (const void *)leaf_fact_ll_kernel<FACT_THREADS, true>;
-    HPL_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), args, 0, st));
+    HPL_CUDA_TRY(launch_grid(wk, fn, G, NT, args, st));
     count_launch();
-    if (w < 0) return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
 cudaError_t launch_leaf_dist(cudaStream_t st, int64_t m, double *P, int64_t ldp, int k0, int w,
                              int64_t *ipiv, FactWork *wk, DistFact *df)
 {
-    if (!g_num_sms) {
-        int dev;
-        HPL_CUDA_TRY(cudaGetDevice(&dev));
-        HPL_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    ensure_sms(wk);
     if (df->dp.jbp > 1024) return cudaErrorInvalidValue;
     int G, NT;
-    leaf_grid(m, wk->max_ctas, &G, &NT);
+    leaf_grid(wk, m, &G, &NT);
     int m_i = (int)m;
     int64_t ldp_ = ldp;
     int k0_ = k0, w_ = w;
     unsigned long long *info = reinterpret_cast<unsigned long long *>(wk->info);
     unsigned long long seq0 = *df->seq;
     unsigned long long *winflag = reinterpret_cast<unsigned long long *>(wk->bar + 8);
+    SpinCtl sc = wk->spin();
     void *args[] = {&m_i, &ldp_, &P, &k0_, &w_, &ipiv, &wk->cand, &wk->win, &wk->tsnap,
-                    &winflag, &wk->bar, &info, &df->dp, &df->ex, &seq0};
+                    &winflag, &wk->bar, &info, &df->dp, &df->ex, &seq0, &sc};
     const void *fn = NT == 32 ? (const void *)leaf_fact_dist_kernel<32>
                               : (const void *)leaf_fact_dist_kernel<FACT_THREADS>;
-    HPL_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), args, 0, st));
+    HPL_CUDA_TRY(launch_grid(wk, fn, G, NT, args, st));
     *df->seq += (unsigned long long)w;
     count_launch();
     return cudaSuccess;
@@ -927,8 +939,8 @@ cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t 
         if (df) return launch_leaf_dist(st, m, P, ldp, c0, w, ipiv, wk, df);  // full-width swaps
         HPL_CUDA_TRY(launch_leaf(st, m, P, ldp, c0, w, ipiv, wk, goff));
         if (nb > w) {
-            panel_laswp_kernel<<<(unsigned)cdiv(nb, 128), 128, 0, st>>>((int)nb, ldp, P, c0, w,
-                                                                       ipiv);
+            panel_laswp_kernel<<<(unsigned)cdiv(nb, 128), 128, 0, st>>>((int)m, (int)nb, ldp, P,
+                                                                       c0, w, ipiv);
             count_launch();
             HPL_CUDA_TRY(cudaGetLastError());
         }
@@ -949,57 +961,31 @@ cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t 
         HPL_CUDA_TRY(rm_to_cm(st, w2, w1, P + (int64_t)(c0 + w1) * ldp + c0, ldp, scratch, lds));
         HPL_CUDA_TRY(dgemm(st, GEMM_UPDATE, false, w2, mrest, w1, scratch, lds,
                            P + (int64_t)c0 * ldp + c0 + w1, ldp,
-                           P + (int64_t)(c0 + w1) * ldp + c0 + w1, ldp, -1, nullptr, 0,
+                           P + (int64_t)(c0 + w1) * ldp + c0 + w1, ldp, wk->gemm_cfg, nullptr, 0,
                            SLOT_FACT));
     }
     return rec_fact(st, m, nb, P, ldp, c0 + w1, w2, ipiv, nbmin, wk, scratch, goff, df);
 }
 
-// a8 as a standalone kernel (tests): the FACT's candidate reduction rule.
-__global__ void maxloc_kernel(int n, const double *absval, const int64_t *row, int64_t *winner)
-{
-    double bv = -1.0;
-    long long br = LLONG_MAX;
-    int bc = -1;
-    for (int c = threadIdx.x; c < n; c += 32)
-        if (better(absval[c], row[c], bv, br)) { bv = absval[c]; br = row[c]; bc = c; }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
-        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (better(ov, orow, bv, br)) { bv = ov; br = orow; bc = oc; }
-    }
-    if (threadIdx.x == 0) *winner = bc;
-}
-
 }  // namespace
 
-cudaError_t maxloc_dev(cudaStream_t st, int n, const double *absval, const int64_t *row,
-                       int64_t *winner)
+void fact_set_leaf_ctas(FactWork *w, int max_ctas, int rows_per_cta)
 {
-    maxloc_kernel<<<1, 32, 0, st>>>(n, absval, row, winner);
-    count_launch();
-    return cudaGetLastError();
-}
-
-void fact_set_leaf_warp_ctas(int ctas) { g_leaf_warp_ctas = ctas; }
-void fact_set_leaf_variant(int v) { g_leaf_variant = (v >= 0 && v <= 2) ? v : 0; }
-void fact_set_leaf_cluster(int on) { g_leaf_cluster = on ? 1 : 0; }
-int fact_get_leaf_variant() { return g_leaf_variant; }
-
-void fact_set_leaf_ctas(int max_ctas, int rows_per_cta)
-{
-    if (max_ctas >= 0) g_leaf_max_ctas = max_ctas;
-    if (rows_per_cta > 0) g_leaf_rows_per_cta = rows_per_cta;
+    if (max_ctas >= 0) w->leaf_max_ctas = max_ctas;
+    if (rows_per_cta > 0) w->leaf_rows_per_cta = rows_per_cta;
 }
 
 cudaError_t fact_work_alloc(FactWork *w)
 {
     w->max_ctas = MAX_CTAS;
+    w->num_sms = 0;
+    w->timeout_ns = 60ull * 1000000000ull;
     HPL_CUDA_TRY(cudaMalloc(&w->cand, sizeof(double) * 2 * (MAX_CTAS + 1) * REC));
-    HPL_CUDA_TRY(cudaMalloc(&w->bar, 64));
-    HPL_CUDA_TRY(cudaMemset(w->bar, 0, 64));
+    // bar: [0] count, [1] generation, bytes 32..39 the distributed leaf's
+    // winner flag, bytes 64..71 the context's abort word (SpinCtl)
+    HPL_CUDA_TRY(cudaMalloc(&w->bar, 128));
+    HPL_CUDA_TRY(cudaMemset(w->bar, 0, 128));
+    w->abort = reinterpret_cast<unsigned long long *>(w->bar + 16);
     HPL_CUDA_TRY(cudaMalloc(&w->info, sizeof(int64_t)));
     HPL_CUDA_TRY(cudaMemset(w->info, 0xff, sizeof(int64_t)));
     HPL_CUDA_TRY(cudaMalloc(&w->win, sizeof(double) * (1024 + 2)));
@@ -1019,6 +1005,7 @@ void fact_work_free(FactWork *w)
     w->cand = nullptr;
     w->bar = nullptr;
     w->info = nullptr;
+    w->abort = nullptr;
 }
 
 cudaError_t fact_gather(cudaStream_t st, int64_t rows, int64_t jb, int64_t j0, int NB, int P,

@@ -45,9 +45,7 @@ struct GemmParams {
     int tiles_m, tiles_n;
     int prefetch_c;
     unsigned zero;       // always 0; opaque to the compiler (see release below)
-    int red_epi;         // UPDATE epilogue as red.global.add.f64 of -acc (no C load)
     int ntiles;          // tiles_m * tiles_n; CTA b owns tiles b, b + gridDim.x, ...
-    int tiles_per_cta;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -65,11 +63,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_addr(uint32_t addr)
@@ -111,11 +104,6 @@ __device__ __forceinline__ double2 lds128(uint32_t addr)
     return v;
 }
 
-__device__ __forceinline__ void red_add(double *p, double v)
-{
-    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0)
 {
     asm volatile(
@@ -147,18 +135,15 @@ struct alignas(64) ParamPad {
     unsigned char b[64 * (SLOT + 1)];
 };
 
-// EPI: 0 = C -= acc through registers (C prefetched to L2), 1 = red.global.add
-// of -acc per element, 2 = -acc staged in shared memory (the drained stage
-// ring) and added to C by one TMA reduce-add of the whole tile
-// (cp.reduce.async.bulk.tensor .add: the L2 performs C + (-acc), one rounding,
-// bitwise equal to C - acc).  EPI 2 needs one tile per CTA.
-template <class C, int SLOT, int EPI>
+// Epilogue: C -= acc through registers, C prefetched to L2 at tile start.
+// (Round 1 measured two alternatives equal and removed them: red.global.add
+// of -acc per element, and -acc staged in the drained ring + one TMA
+// reduce-add of the tile — DESIGN.md §9.)
+template <class C, int SLOT>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
 dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
-                 const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmC)
+                 const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB)
 {
-    constexpr bool RED = EPI == 1;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -234,7 +219,7 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     const int row_base = m0 + wm * C::WM;   // first row of this warp's tile
     const int col_base = n0 + wn * C::WN;
 
-    if (EPI != 2 && p.prefetch_c && p.mode == GEMM_UPDATE) {
+    if (p.prefetch_c && p.mode == GEMM_UPDATE) {
         // Pull this warp's C tile toward L2 while the mainloop runs: each lane
         // touches the 128-byte lines of its own rows.
         for (int r = lane; r < C::WM; r += 32) {
@@ -299,37 +284,6 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     }
 
     // ================= epilogue: C -= acc  (or C = acc) =================
-    if constexpr (EPI == 2) {
-        // every consumer has finished reading the ring (the producer issued
-        // exactly this tile's stages, all consumed): reuse it for the tile
-        asm volatile("bar.sync 1, %0;" ::"n"(C::NCW * 32) : "memory");
-        double *stile = reinterpret_cast<double *>(smem);
-#pragma unroll
-        for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = wm * C::WM + 16 * i + 2 * g + h;
-#pragma unroll
-                for (int j = 0; j < C::NJ; ++j) {
-                    const int cc = wn * C::WN + 16 * j + 4 * t;
-                    double2 *q = reinterpret_cast<double2 *>(stile + r * C::BN + cc);
-                    q[0] = make_double2(-acc[i][j][0][2 * h], -acc[i][j][1][2 * h]);
-                    q[1] = make_double2(-acc[i][j][0][2 * h + 1], -acc[i][j][1][2 * h + 1]);
-                }
-            }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, %0;" ::"n"(C::NCW * 32) : "memory");
-        if (warp == 0 && lane == 0) {
-            asm volatile(
-                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
-                " [%0, {%1, %2}], [%3];" ::"l"(reinterpret_cast<uint64_t>(&tmC)),
-                "r"(n0), "r"(m0), "r"(smem_base)
-                : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        continue;
-    }
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
 #pragma unroll
@@ -343,14 +297,7 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
                 // row 2g: lo.c0 hi.c0 lo.c1 hi.c1 ; row 2g+1: lo.c2 hi.c2 lo.c3 hi.c3
                 const double v0 = acc[i][j][0][2 * h], v1 = acc[i][j][1][2 * h];
                 const double v2 = acc[i][j][0][2 * h + 1], v3 = acc[i][j][1][2 * h + 1];
-                if (RED && p.mode == GEMM_UPDATE) {
-                    // C + (-acc) performed at L2: one rounding, as C - acc; the
-                    // warp does not wait for C (each element is touched once)
-                    if (col + 0 < p.n) red_add(crow + col + 0, -v0);
-                    if (col + 1 < p.n) red_add(crow + col + 1, -v1);
-                    if (col + 2 < p.n) red_add(crow + col + 2, -v2);
-                    if (col + 3 < p.n) red_add(crow + col + 3, -v3);
-                } else if (vec_ok && col + 3 < p.n) {
+                if (vec_ok && col + 3 < p.n) {
                     double2 *q = reinterpret_cast<double2 *>(crow + col);
                     if (p.mode == GEMM_UPDATE) {
                         double2 x0 = q[0], x1 = q[1];
@@ -422,59 +369,28 @@ cudaError_t make_map(CUtensorMap *map, const double *base, int64_t xext, int64_t
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// C (row-major, ld doubles) for the TMA reduce-add epilogue: box = one tile,
-// no swizzle (the staged tile is dense row-major in shared memory).
-cudaError_t make_map_c(CUtensorMap *map, const double *base, int64_t ncols, int64_t nrows,
-                       int64_t ld, int box_cols, int box_rows)
-{
-    EncodeFn enc = get_encode();
-    if (!enc) return cudaErrorNotSupported;
-    cuuint64_t gdim[2] = {(cuuint64_t)ncols, (cuuint64_t)nrows};
-    cuuint64_t gstr[1] = {(cuuint64_t)(ld * 8)};
-    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), gdim,
-                     gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
 // 128x64 tile, 4 consumer warps (64x32 each), 2 CTAs/SM, 4 stages.
 using CfgA = Cfg<128, 64, 64, 32, 4, 2>;
 // 128x128 tile, 8 consumer warps (64x32 each), 1 CTA/SM, 6 stages.
 using CfgB = Cfg<128, 128, 64, 32, 6, 1>;
-// 64x64 tile, 4 consumer warps (32x32), 3 CTAs/SM (small/tail problems).
+// 64x64 tile, 4 consumer warps (32x32), 3 CTAs/SM: the default.
+// Round 1 measured 6-stage, 4-CTA/SM and 8-warp 64x64 variants slower and
+// removed them (profiles/r01_gemm_cfg_probe.log).
 using CfgC = Cfg<64, 64, 32, 32, 4, 3>;
-// 64x64 tile, 2 CTAs/SM, 6 stages (tuning variant).
-using CfgD = Cfg<64, 64, 32, 32, 6, 2>;
-// 64x64 tile, 4 CTAs/SM, 3 stages (more warps to cover epilogues).
-using CfgE = Cfg<64, 64, 32, 32, 3, 4>;
-// 64x64 tile, 8 consumer warps (32x16 each), 3 CTAs/SM: 6 DMMA warps per SM
-// sub-partition instead of 3 (more issue slack, 1.5x the LDS bytes per DMMA).
-using CfgF = Cfg<64, 64, 32, 16, 4, 3>;
-// 64x64 tile, 8 consumer warps (32x16), 2 CTAs/SM, 6 stages.
-using CfgG = Cfg<64, 64, 32, 16, 6, 2>;
 
-int g_default_cfg = 2;
-int g_tiles_per_cta = 1;
-int g_red_epi = 0;
-
-// The RED and TMA-reduce epilogues are separate instantiations (default
-// config only): a runtime branch in the epilogue made the default kernel spill.
-template <class C, int SLOT, int EPI = 0>
+template <class C, int SLOT>
 cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
-                        const GemmParams &p, const CUtensorMap *mc = nullptr)
+                        const GemmParams &p)
 {
-    static bool attr_set = false;
-    if (!attr_set) {
-        HPL_CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT, EPI>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set = true;
-    }
-    const long long grid = cdiv(p.ntiles, p.tiles_per_cta);
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    });
+    HPL_CUDA_TRY(attr_err);
     ParamPad<SLOT> pad{};
-    const CUtensorMap &mcr = mc ? *mc : ma;   // unused unless EPI == 2
-    dgemm_tma_kernel<C, SLOT, EPI><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb, mcr);
+    dgemm_tma_kernel<C, SLOT><<<(unsigned)p.ntiles, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
     count_launch();
     return cudaGetLastError();
 }
@@ -485,39 +401,16 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
 {
     p.tiles_m = (int)cdiv(p.m, C::BM);
     p.tiles_n = (int)cdiv(p.n, C::BN);
-    p.ntiles = p.tiles_m * p.tiles_n;
-    // several tiles per CTA only for large grids (short kernels keep one tile
-    // per CTA so concurrent FACT kernels find free SM slots quickly)
-    p.tiles_per_cta = p.ntiles >= 16 * 148 * C::MINB ? g_tiles_per_cta : 1;
-    if constexpr (std::is_same_v<C, CfgC>) {
-        if (p.red_epi == 2 && p.mode == GEMM_UPDATE && p.C2 == nullptr &&
-            (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.ldc & 1) == 0) {
-            // TMA reduce-add epilogue: one tile per CTA, a C tensor map (box = tile)
-            CUtensorMap mc;
-            HPL_CUDA_TRY(make_map_c(&mc, p.C, p.n, p.m, p.ldc, C::BN, C::BM));
-            p.tiles_per_cta = 1;
-            switch (slot) {
-            case 1: return launch_slot<C, 1, 2>(st, ma, mb, p, &mc);
-            case 2: return launch_slot<C, 2, 2>(st, ma, mb, p, &mc);
-            default: return launch_slot<C, 0, 2>(st, ma, mb, p, &mc);
-            }
-        }
-        if (p.red_epi == 1 && p.mode == GEMM_UPDATE && slot == 0)
-            return launch_slot<C, 0, 1>(st, ma, mb, p);
-    }
+    p.ntiles = p.tiles_m * p.tiles_n;     // one tile per CTA
     switch (slot) {
-    case 1: return launch_slot<C, 1>(st, ma, mb, p);
-    case 2: return launch_slot<C, 2>(st, ma, mb, p);
-    default: return launch_slot<C, 0>(st, ma, mb, p);
+    case SLOT_LOOKAHEAD: return launch_slot<C, SLOT_LOOKAHEAD>(st, ma, mb, p);
+    case SLOT_FACT: return launch_slot<C, SLOT_FACT>(st, ma, mb, p);
+    case SLOT_RS: return launch_slot<C, SLOT_RS>(st, ma, mb, p);
+    default: return launch_slot<C, SLOT_TRAIL>(st, ma, mb, p);
     }
 }
 
 }  // namespace
-
-void dgemm_set_default_cfg(int cfg) { g_default_cfg = cfg; }
-void dgemm_set_tiles_per_cta(int t) { g_tiles_per_cta = t > 0 ? t : 1; }
-void dgemm_set_red_epilogue(int on) { g_red_epi = on; }
-int dgemm_get_default_cfg() { return g_default_cfg; }
 
 cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n, int64_t k,
                   const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
@@ -550,16 +443,12 @@ cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n,
     p.C2 = C2; p.ldc2 = ldc2;
     p.prefetch_c = 1;
     p.zero = 0;
-    p.red_epi = g_red_epi;
-    if (cfg < 0) cfg = g_default_cfg;
+    if (cfg < 0) cfg = DGEMM_DEFAULT_CFG;
     switch (cfg) {
+    case 0: return launch_cfg<CfgA>(st, ma, mb, p, slot);
     case 1: return launch_cfg<CfgB>(st, ma, mb, p, slot);
     case 2: return launch_cfg<CfgC>(st, ma, mb, p, slot);
-    case 3: return launch_cfg<CfgD>(st, ma, mb, p, slot);
-    case 4: return launch_cfg<CfgE>(st, ma, mb, p, slot);
-    case 5: return launch_cfg<CfgF>(st, ma, mb, p, slot);
-    case 6: return launch_cfg<CfgG>(st, ma, mb, p, slot);
-    default: return launch_cfg<CfgA>(st, ma, mb, p, slot);
+    default: return cudaErrorInvalidValue;
     }
 }
 

@@ -1,10 +1,11 @@
 // kernels_misc.cu — generator (a11), panel copies, column TRSM / unit-lower
 // inverse (a4 helper), back substitution (a10) and the scaled residual (a11).
 #include "hpl_internal.cuh"
+#include <math_constants.h>
 
 namespace hpl {
 
-std::atomic<int64_t> g_launches{0};
+thread_local int64_t t_launches = 0;
 
 // ---------------------------------------------------------------- generator
 // Entry (i, j) of the seeded N x (N+1) system [A | b]: SplitMix64 of the
@@ -445,7 +446,14 @@ __global__ void residual_partial_kernel(uint64_t seed, int64_t N, int NB, int P,
 }
 
 // out4 = {max|r_l - b_gi|, max a_l, max|x_i|, max|b_i|} over local rows
-// (x over all N: it is replicated).  out4 zeroed here.
+// (x over all N: it is replicated).  out4 zeroed here.  A non-finite value
+// enters as +inf: fmax would drop a NaN, and an x with a NaN entry would then
+// give the residual 0 — here it makes the residual +inf (fails).
+__device__ __forceinline__ double fin_or_inf(double v)
+{
+    return isfinite(v) ? v : CUDART_INF;
+}
+
 __global__ void residual_finalize_kernel(uint64_t seed, int64_t N, int NB, int P, int myrow,
                                          int64_t mloc, const double *__restrict__ r,
                                          const double *__restrict__ a,
@@ -456,12 +464,12 @@ __global__ void residual_finalize_kernel(uint64_t seed, int64_t N, int NB, int P
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < mloc; l += stride) {
         const int64_t i = l2g(l, NB, P, myrow);
         const double b = hpl_entry(seed, (uint64_t)N, (uint64_t)i, (uint64_t)N);
-        m0 = fmax(m0, fabs(r[l] - b));
-        m1 = fmax(m1, a[l]);
-        m3 = fmax(m3, fabs(b));
+        m0 = fmax(m0, fin_or_inf(fabs(r[l] - b)));
+        m1 = fmax(m1, fin_or_inf(a[l]));
+        m3 = fmax(m3, fin_or_inf(fabs(b)));
     }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += stride)
-        m2 = fmax(m2, fabs(x[i]));
+        m2 = fmax(m2, fin_or_inf(fabs(x[i])));
     for (int o = 16; o; o >>= 1) {
         m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
         m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
@@ -488,11 +496,15 @@ cudaError_t residual_partial(cudaStream_t st, uint64_t seed, int64_t N, int NB, 
     return cudaGetLastError();
 }
 
+__global__ void zero4_kernel(double *p) { p[threadIdx.x] = 0.0; }
+
 cudaError_t residual_finalize(cudaStream_t st, uint64_t seed, int64_t N, int NB, int P, int myrow,
                               int64_t mloc, const double *r, const double *a, const double *x,
                               double *out4)
 {
-    HPL_CUDA_TRY(cudaMemsetAsync(out4, 0, 4 * sizeof(double), st));
+    // (a kernel, not a memset: no copy-engine work between the collectives)
+    zero4_kernel<<<1, 4, 0, st>>>(out4);
+    count_launch();
     residual_finalize_kernel<<<296, 256, 0, st>>>(seed, N, NB, P, myrow, mloc, r, a, x, out4);
     count_launch();
     return cudaGetLastError();

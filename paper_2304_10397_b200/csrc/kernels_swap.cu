@@ -19,9 +19,13 @@ namespace {
 
 constexpr int HSLOTS = 2048;  // open-addressing table for rows below the block (jb <= 1024)
 
+// A pivot outside [r0 + k, nrows) cannot come from a FACT that completed; it
+// only appears after a peer timeout abandoned the leaf (hpl_internal.cuh
+// SpinCtl).  It is treated as "no interchange" so no later kernel indexes
+// outside the matrix; the context reports HPL_ERR_PEER.
 __global__ void pivot_plan_kernel(int jb, long long r0, const int64_t *__restrict__ ipiv_rel,
-                                  long long goff, int64_t *gpiv, int64_t *src, int64_t *disp,
-                                  int *ndisp)
+                                  long long goff, long long nrows, int64_t *gpiv, int64_t *src,
+                                  int64_t *disp, int *ndisp)
 {
     __shared__ long long keys[HSLOTS];
     __shared__ long long vals[HSLOTS];
@@ -29,12 +33,14 @@ __global__ void pivot_plan_kernel(int jb, long long r0, const int64_t *__restric
     for (int i = threadIdx.x; i < HSLOTS; i += blockDim.x) keys[i] = -1;
     for (int k = threadIdx.x; k < jb; k += blockDim.x) {
         cur[k] = r0 + k;
-        gpiv[k] = ipiv_rel[k] + goff;
+        const long long rel = ipiv_rel[k];
+        gpiv[k] = (rel >= k && r0 + rel < nrows ? rel : k) + goff;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int k = 0; k < jb; ++k) {
-            const long long p = r0 + ipiv_rel[k];
+            const long long rel = ipiv_rel[k];
+            const long long p = rel >= k && r0 + rel < nrows ? r0 + rel : r0 + k;
             if (p == r0 + k) continue;
             if (p < r0 + jb) {
                 const long long t = cur[k];
@@ -166,40 +172,30 @@ rs_scatter_kernel(const int64_t *__restrict__ disp, const int *__restrict__ ndis
 // displaced rows this process owns — the original block row they receive,
 // from the owner of block row j, into W.  Phase 2 (after a second barrier:
 // every peer has finished reading) is rs_scatter from W.
-__device__ __forceinline__ unsigned long long rs_ld_acquire_sys(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void rs_st_release_sys(unsigned long long *p, unsigned long long v)
-{
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// lane p < P: announce arrival at `slot` to peer p, then wait for peer p's arrival.
-__global__ void rs_barrier_kernel(RsPeers pr, int slot, unsigned long long value)
+// lane p < P: announce arrival at `slot` to peer p, then wait (bounded) for
+// peer p's arrival.
+__global__ void rs_barrier_kernel(RsPeers pr, int slot, unsigned long long value, SpinCtl sc)
 {
     const int p = threadIdx.x;
     if (p >= pr.P) return;
     __threadfence_system();
-    rs_st_release_sys(pr.flag[p] + (size_t)slot * MAX_P + pr.myrow, value);
-    while (rs_ld_acquire_sys(pr.my_flag + (size_t)slot * MAX_P + p) < value) __nanosleep(64);
+    st_release_sys(pr.flag[p] + (size_t)slot * MAX_P + pr.myrow, value);
+    spin_geq_sys(pr.my_flag + (size_t)slot * MAX_P + p, value, sc,
+                 SITE_RS_BARRIER | (unsigned long long)slot << 4 | (unsigned long long)p << 8);
     __threadfence_system();
 }
 
 // Generic flag step (LBCAST over peer memory): lanes < nsig publish sv to
 // sig[lane] (after a system fence: this stream's earlier writes are visible
-// first); lanes < nwait spin until *wt[lane] >= wv.
-__global__ void flag_kernel(FlagOp op)
+// first); lanes < nwait wait (bounded) until *wt[lane] >= wv.
+__global__ void flag_kernel(FlagOp op, SpinCtl sc)
 {
     const int l = threadIdx.x;
     if (l < op.nsig) {
         __threadfence_system();
-        rs_st_release_sys(op.sig[l], op.sv);
+        st_release_sys(op.sig[l], op.sv);
     }
-    if (l < op.nwait)
-        while (rs_ld_acquire_sys(op.wt[l]) < op.wv) __nanosleep(128);
+    if (l < op.nwait) spin_geq_sys(op.wt[l], op.wv, sc, SITE_FLAG | (unsigned long long)l << 8);
     __threadfence_system();
 }
 
@@ -288,10 +284,11 @@ cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, c
     return cudaGetLastError();
 }
 
-cudaError_t rs_barrier(cudaStream_t st, const RsPeers &pr, int slot, unsigned long long value)
+cudaError_t rs_barrier(cudaStream_t st, const RsPeers &pr, int slot, unsigned long long value,
+                       const SpinCtl &sc)
 {
     if (pr.P < 1 || pr.P > MAX_P || slot < 0 || slot >= RS_SLOTS) return cudaErrorInvalidValue;
-    rs_barrier_kernel<<<1, 32, 0, st>>>(pr, slot, value);
+    rs_barrier_kernel<<<1, 32, 0, st>>>(pr, slot, value, sc);
     count_launch();
     return cudaGetLastError();
 }
@@ -312,31 +309,31 @@ cudaError_t rs_gather_peer(cudaStream_t st, int64_t jb, const int64_t *src, cons
     return cudaGetLastError();
 }
 
-cudaError_t flag_op(cudaStream_t st, const FlagOp &op)
+cudaError_t flag_op(cudaStream_t st, const FlagOp &op, const SpinCtl &sc)
 {
     if (op.nsig < 0 || op.nsig > 32 || op.nwait < 0 || op.nwait > 32) return cudaErrorInvalidValue;
     if (op.nsig == 0 && op.nwait == 0) return cudaSuccess;
-    flag_kernel<<<1, 32, 0, st>>>(op);
+    flag_kernel<<<1, 32, 0, st>>>(op, sc);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t pivot_plan(cudaStream_t st, int64_t jb, int64_t r0, const int64_t *ipiv_rel,
-                       int64_t goff, int64_t *gpiv, int64_t *src, int64_t *disp, int *ndisp)
+                       int64_t goff, int64_t nrows, int64_t *gpiv, int64_t *src, int64_t *disp,
+                       int *ndisp)
 {
     if (jb <= 0) return cudaSuccess;
     if (jb > 1024) return cudaErrorInvalidValue;
-    pivot_plan_kernel<<<1, 256, 0, st>>>((int)jb, r0, ipiv_rel, goff, gpiv, src, disp, ndisp);
+    pivot_plan_kernel<<<1, 256, 0, st>>>((int)jb, r0, ipiv_rel, goff, nrows, gpiv, src, disp,
+                                         ndisp);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src,
-                                 const int64_t *disp, const int *ndisp, int64_t max_disp,
-                                 double *A, int64_t lda, int64_t c0, int64_t c1, double *U,
-                                 int64_t ldu)
+                                 const int64_t *disp, const int *ndisp, double *A, int64_t lda,
+                                 int64_t c0, int64_t c1, double *U, int64_t ldu)
 {
-    (void)max_disp;
     if (jb <= 0 || c1 <= c0) return cudaSuccess;
     const int vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda & 1) == 0 &&
                      (c0 & 1) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&

@@ -15,7 +15,7 @@ import numpy as np
 from ._lib import lib, ptr
 
 STATUS = {0: "HPL_OK", 1: "HPL_ERR_ARG", 2: "HPL_ERR_STATE", 3: "HPL_ERR_OOM",
-          4: "HPL_ERR_CUDA", 5: "HPL_ERR_NCCL", 6: "HPL_ERR_SINGULAR"}
+          4: "HPL_ERR_CUDA", 5: "HPL_ERR_NCCL", 6: "HPL_ERR_SINGULAR", 7: "HPL_ERR_PEER"}
 
 
 class HplError(RuntimeError):
@@ -88,6 +88,56 @@ def hpl_init_dist(N: int, NB: int, P: int, Q: int, seed: int, rank: int, nranks:
             lib.hpl_free(h)
         raise HplError(st, msg)
     return Ctx(h.value, N, NB, P, Q, seed)
+
+
+def hpl_init_loopback(N: int, NB: int, P: int, Q: int, seed: int = 42, device: int = 0) -> list:
+    """The P*Q rank contexts of one grid on one device of this process
+    (include/hpl.h hpl_init_loopback); drive them with run_ranks."""
+    nr = P * Q
+    hs = (ctypes.c_void_p * nr)()
+    st = lib.hpl_init_loopback(N, NB, P, Q, seed, device, hs)
+    ctxs = [Ctx(h, N, NB, P, Q, seed) if h else None for h in hs]
+    if st != 0:
+        msg = next((lib.hpl_last_error(c.h).decode(errors="replace") for c in ctxs
+                    if c is not None and lib.hpl_last_error(c.h)), "")
+        if not msg and st == 2:
+            msg = ("needs CUDA_MODULE_LOADING=EAGER and CUDA_DEVICE_MAX_CONNECTIONS >= 3*P*Q "
+                   "before CUDA initialises")
+        for c in ctxs:
+            if c is not None:
+                hpl_free(c)
+        raise HplError(st, msg or "invalid argument")
+    return ctxs
+
+
+def run_ranks(fn, ctxs: list) -> list:
+    """Call fn(ctx) for every rank context concurrently, one host thread per
+    rank (ctypes releases the GIL during the library call), and return the
+    results in rank order; the first exception raised by a rank is re-raised
+    after every thread has finished."""
+    import threading
+    out = [None] * len(ctxs)
+    err = [None] * len(ctxs)
+
+    def body(r):
+        try:
+            out[r] = fn(ctxs[r])
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(len(ctxs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    bad = [(r, e) for r, e in enumerate(err) if e is not None]
+    if bad:
+        # the first failing rank's exception, with every rank's message attached
+        e = bad[0][1]
+        if len(bad) > 1 and isinstance(e, HplError):
+            e.args = (e.args[0] + " | " + "; ".join(f"rank {r}: {x}" for r, x in bad[1:]),)
+        raise e
+    return out
 
 
 def hpl_factor(ctx: Ctx) -> None:
@@ -173,6 +223,14 @@ def hpl_last_timing(ctx: Ctx) -> dict:
                 dgemm_flop=o[4], launches=int(o[5]))
 
 
+def hpl_phase_stats(ctx: Ctx) -> dict:
+    """Per-phase totals of the last factor/solve (include/hpl.h hpl_phase_stats)."""
+    o = np.zeros(8, dtype=np.float64)
+    ctx.check(lib.hpl_phase_stats(ctx.h, ptr(o)))
+    return dict(laswp_ms=o[0], laswp_bytes=o[1], trsm_ms=o[2], trsm_flop=o[3], fact_ms=o[4],
+                solve_ms=o[5], solve_bytes=o[6], dgemm_ms=o[7])
+
+
 def hpl_plan_iteration(N: int, NB: int, P: int, Q: int, myrow: int, mycol: int, j: int) -> dict:
     """Host-only bookkeeping of iteration j on process (myrow, mycol)."""
     o = np.zeros(8, dtype=np.int64)
@@ -226,13 +284,16 @@ def hplk_trsm(L, B):
     return B
 
 
-def hplk_panel_fact(Pn, nbmin: int = 16):
-    """Device panel LU of an m x nb panel. Returns (LU, ipiv, info)."""
+def hplk_panel_fact(Pn, nbmin: int = 16, leaf_variant: int = 0, leaf_cluster: int = 1,
+                    leaf_ctas: int = 0):
+    """Device panel LU of an m x nb panel with the chosen pivot-picking leaf
+    (include/hpl_kernels.h). Returns (LU, ipiv, info)."""
     P_cm = np.array(Pn, dtype=np.float64, order="F", copy=True)
     m, nb = P_cm.shape
     ipiv = np.zeros(nb, dtype=np.int64)
     info = ctypes.c_int64(-1)
-    st = lib.hplk_panel_fact(m, nb, ptr(P_cm), m, ptr(ipiv), nbmin, ctypes.byref(info))
+    st = lib.hplk_panel_fact(m, nb, ptr(P_cm), m, ptr(ipiv), nbmin, leaf_variant, leaf_cluster,
+                             leaf_ctas, ctypes.byref(info))
     if st not in (0, -2):
         _k(st, "hplk_panel_fact")
     return np.ascontiguousarray(P_cm), ipiv, int(info.value)
@@ -268,12 +329,18 @@ def hplk_generate(seed: int, N: int, i0: int, rows: int, j0: int, cols: int):
     return out
 
 
-def hplk_maxloc(absval, rows):
-    a = np.ascontiguousarray(absval, dtype=np.float64)
-    r = np.ascontiguousarray(rows, dtype=np.int64)
-    w = ctypes.c_int64(-1)
-    _k(lib.hplk_maxloc(len(a), ptr(a), ptr(r), ctypes.byref(w)), "hplk_maxloc")
-    return float(a[w.value]), int(r[w.value])
+def hplk_residual(seed: int, N: int, x, want_rows: bool = False):
+    """Device scaled residual of the seeded system for x (the hpl_residual
+    kernels).  Returns (resid, out4) or, with want_rows, (resid, out4, rsum, asum)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out4 = np.zeros(4, dtype=np.float64)
+    r = ctypes.c_double()
+    rs = np.empty(N, dtype=np.float64) if want_rows else None
+    as_ = np.empty(N, dtype=np.float64) if want_rows else None
+    _k(lib.hplk_residual(seed, N, ptr(x), ptr(rs) if want_rows else None,
+                         ptr(as_) if want_rows else None, ptr(out4), ctypes.byref(r)),
+       "hplk_residual")
+    return (float(r.value), out4, rs, as_) if want_rows else (float(r.value), out4)
 
 
 def hplk_dgemm_bench(m: int, n: int, k: int, cfg: int = -1, reps: int = 5) -> np.ndarray:

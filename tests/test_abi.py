@@ -68,6 +68,26 @@ def test_invalid_args_rejected_without_gpu_work():
         assert not h.value
 
 
+def test_loopback_refuses_without_concurrency_env():
+    """hpl_init_loopback (P*Q > 1) needs CUDA_MODULE_LOADING=EAGER and enough
+    hardware queues set before CUDA initialises (its ranks' kernels wait on
+    each other): without them it returns HPL_ERR_STATE before any GPU work;
+    invalid grids are HPL_ERR_ARG."""
+    import ctypes
+    import subprocess
+    import sys
+    code = ("import ctypes,sys; from paper_2304_10397_b200 import _lib;"
+            "h=(ctypes.c_void_p*4)();"
+            "print(_lib.lib.hpl_init_loopback(1024,64,2,2,1,0,h),"
+            "_lib.lib.hpl_init_loopback(1024,64,9,1,1,0,h),"
+            "_lib.lib.hpl_init_loopback(1024,33,2,2,1,0,h), all(not v for v in h))")
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("CUDA_MODULE_LOADING", "CUDA_DEVICE_MAX_CONNECTIONS")}
+    env["PYTHONPATH"] = ROOT
+    out = subprocess.check_output([sys.executable, "-c", code], env=env, text=True).split()
+    assert out == ["2", "1", "1", "True"]
+
+
 def test_hot_kernels_do_not_spill():
     """The trailing-update DGEMM (default 64x64 config, every stream slot) and
     the distributed leaf keep everything in registers: a local-memory stack

@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 import oracle
-from hpl_inputs import hpl_panel, random_ipiv, random_unit_lower, upper_well_conditioned
+from hpl_inputs import (hpl_panel, integer_panel, random_ipiv, random_unit_lower, twin_panel,
+                        upper_well_conditioned)
 from tests import brute
 
 pytestmark = pytest.mark.gpu
@@ -29,17 +30,6 @@ def test_generator_bitwise(H, N, i0, rows, j0, cols):
     o = np.array([[oracle.gen_entry(42, N, i, j) for j in range(j0, j0 + cols)]
                   for i in range(i0, i0 + rows)])
     assert np.array_equal(g, o)
-
-
-# ------------------------------------------------------------------ a8 maxloc
-def test_maxloc(H):
-    assert H.hplk_maxloc([1.0, 9.0, 3.0, 9.0], [10, 7, 2, 3]) == (9.0, 3)
-    assert H.hplk_maxloc([4.0, 4.0], [9, 1]) == (4.0, 1)
-    rng = np.random.default_rng(0)
-    for n in (1, 5, 33, 148, 1000):
-        v = np.abs(rng.integers(0, 4, n).astype(np.float64))  # many ties
-        r = rng.permutation(10 * n)[:n]
-        assert H.hplk_maxloc(v, r) == oracle.maxloc(v, r)
 
 
 # ------------------------------------------------------------------ a5/a6 DGEMM
@@ -108,12 +98,7 @@ def test_panel_fact_leaf_variants(H, variant, m, nb, nbmin):
     oracle, and bitwise against the right-looking leaf (same FMA sequences)."""
     Pn = hpl_panel(m, nb, seed=3 * m + nb)
     LU0, ip0, _ = H.hplk_panel_fact(Pn, nbmin=nbmin)
-    with H.hpl_init(64, 16, 1, 1, 1) as ctx:   # the knob is process-wide
-        H.hpl_set_option(ctx, "leaf_variant", variant)
-        try:
-            LU, ipiv, info = H.hplk_panel_fact(Pn, nbmin=nbmin)
-        finally:
-            H.hpl_set_option(ctx, "leaf_variant", 0)
+    LU, ipiv, info = H.hplk_panel_fact(Pn, nbmin=nbmin, leaf_variant=variant)
     LUo, ipo, _ = oracle.getrf(Pn)
     assert info == -1 and np.array_equal(ipiv, ipo)
     assert np.max(np.abs(LU - LUo)) <= 1e-12
@@ -125,11 +110,8 @@ def test_leaf_variant_end_to_end(H):
     def run(v):
         with H.hpl_init(3000, 128, 1, 1, 31) as ctx:
             H.hpl_set_option(ctx, "leaf_variant", v)
-            try:
-                H.hpl_factor(ctx)
-                return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
-            finally:
-                H.hpl_set_option(ctx, "leaf_variant", 0)
+            H.hpl_factor(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
     x0, p0, _ = run(0)
     for v in (1, 2):
         x, p, r = run(v)
@@ -144,12 +126,7 @@ def test_panel_fact_cluster_leaf(H, m, nb, nbmin):
     against the oracle and bitwise against the grid leaf (leaf_cluster=0)."""
     Pn = hpl_panel(m, nb, seed=7 * m + nb)
     LU1, ip1, info1 = H.hplk_panel_fact(Pn, nbmin=nbmin)
-    with H.hpl_init(64, 16, 1, 1, 1) as ctx:   # the knob is process-wide
-        H.hpl_set_option(ctx, "leaf_cluster", 0)
-        try:
-            LU0, ip0, info0 = H.hplk_panel_fact(Pn, nbmin=nbmin)
-        finally:
-            H.hpl_set_option(ctx, "leaf_cluster", 1)
+    LU0, ip0, info0 = H.hplk_panel_fact(Pn, nbmin=nbmin, leaf_cluster=0)
     LUo, ipo, _ = oracle.getrf(Pn)
     assert info1 == -1 and info0 == -1 and np.array_equal(ip1, ipo)
     assert np.max(np.abs(LU1 - LUo)) <= 1e-12
@@ -162,11 +139,8 @@ def test_cluster_leaf_end_to_end(H):
     def run(v):
         with H.hpl_init(6000, 256, 1, 1, 37) as ctx:
             H.hpl_set_option(ctx, "leaf_cluster", v)
-            try:
-                H.hpl_factor(ctx)
-                return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
-            finally:
-                H.hpl_set_option(ctx, "leaf_cluster", 1)
+            H.hpl_factor(ctx)
+            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
     xa, pa, _ = run(0)
     xb, pb, rb = run(1)
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
@@ -179,6 +153,36 @@ def test_panel_fact_special(H):
     Pn[:, 9] = 0.0     # exact zero column -> singular at 9 (reading A3)
     _, _, info = H.hplk_panel_fact(Pn)
     assert info == 9
+
+
+LEAVES = [dict(), dict(leaf_cluster=0), dict(leaf_cluster=0, leaf_ctas=3),
+          dict(leaf_cluster=0, leaf_ctas=1), dict(leaf_variant=1), dict(leaf_variant=2)]
+
+
+@pytest.mark.parametrize("leaf", LEAVES, ids=["cluster", "grid", "grid3", "grid1", "left", "crout"])
+@pytest.mark.parametrize("m,nb,kind", [(1000, 64, "twin"), (3000, 128, "twin"), (777, 34, "twin"),
+                                       (40000, 64, "twin"), (600, 32, "int"), (26000, 64, "int")])
+def test_pivot_ties_through_leaves(H, leaf, m, nb, kind):
+    """a8 pivot rule (max |v|, ties -> smallest row)
+    exercised by the kernels that pick the pivots — the cluster leaf, the
+    grid leaf with 1 / 3 / all CTAs, the left-looking and Crout leaves.
+    "twin": pairs of rows that are exact negations of each other, far apart
+    (different CTAs / cluster ranks), carry every column's maximum; both
+    sides update a pair symmetrically, so each pivot is an exact tie and the
+    full pivot sequence must equal the oracle's.  "int": small integers, so
+    the first column's maximum is shared by many rows across the whole
+    panel; only that first pivot is free of rounding (later equalities
+    depend on the update's rounding order), so only it is compared."""
+    Pn = twin_panel(m, nb, seed=m + nb) if kind == "twin" else integer_panel(m, nb, seed=m)
+    LU, ipiv, info = H.hplk_panel_fact(Pn, nbmin=16, **leaf)
+    LUo, ipo, info_o = oracle.getrf(Pn)
+    if kind == "int":
+        first = int(np.flatnonzero(np.abs(Pn[:, 0]) == np.max(np.abs(Pn[:, 0])))[0])
+        assert ipiv[0] == ipo[0] == first
+        return
+    assert info == info_o == -1
+    assert np.array_equal(ipiv, ipo), int(np.argmax(ipiv != ipo))
+    assert np.max(np.abs(LU - LUo)) <= 1e-12
 
 
 # ------------------------------------------------------------------ a1/a3 LASWP
@@ -218,6 +222,76 @@ def test_back_solve_vs_oracle(H, N, NB):
     ref, info = oracle.back_solve(Uu, y)
     assert info == -1
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ a11 residual
+@pytest.mark.parametrize("N", [256, 3000])
+def test_residual_kernel_unit_vectors(H, N):
+    """x = e_k: every row of A0 x - b0 is ONE product and one subtraction of
+    grid values (exact in binary on both sides), so the device residual rows
+    equal the oracle's bit for bit; ||x|| and ||b0|| exact, ||A0|| (a sum of
+    N magnitudes, order-dependent) within gamma_N; resid within 2 gamma_N."""
+    for k in (0, N // 3, N - 1):
+        x = np.zeros(N)
+        x[k] = 1.0
+        resid, out4, rsum, asum = H.hplk_residual(42, N, x, want_rows=True)
+        b = H.hplk_generate(42, N, 0, N, N, 1)[:, 0]
+        rows = np.arange(N)
+        rr, rowsum = oracle.residual_rows(N, 42, x, rows)
+        assert np.array_equal(rsum - b, rr)
+        assert np.all(np.abs(asum - rowsum) <= brute.gamma(N) * rowsum)
+        ro, po = oracle.residual_seeded(N, 42, x)
+        assert out4[0] == po[0] and out4[2] == po[2] == 1.0 and out4[3] == po[3]
+        assert abs(out4[1] - po[1]) <= brute.gamma(N) * po[1]
+        assert abs(resid - ro) <= 2 * brute.gamma(N) * ro
+
+
+@pytest.mark.parametrize("N,NB", [(256, 32), (8192, 256)])
+def test_residual_vs_oracle_same_x(H, N, NB):
+    """SPEC.md l.383-391 two ways on the SAME x: hpl_residual (the ABI call)
+    equals the kernel hook bitwise (same kernels), and agrees with the
+    oracle's residual of the device x within the bound of two independent
+    length-N dot products (|dr_i| <= 2 gamma_{N+1} (sum|a_ij| ||x|| + |b_i|)).
+    With x perturbed by 1e-2 the residual has no cancellation:
+    both sides agree to 1e-10 relative and fail the < 16 test."""
+    with H.hpl_init(N, NB, 1, 1, 42) as ctx:
+        H.hpl_factor(ctx)
+        x = H.hpl_solve(ctx)
+        r_abi = H.hpl_residual(ctx)
+    r_k, out4, rsum, asum = H.hplk_residual(42, N, x, want_rows=True)
+    assert r_abi == r_k < 16
+    ro, po = oracle.residual_seeded(N, 42, x)
+    b = H.hplk_generate(42, N, 0, N, N, 1)[:, 0]
+    rr, rowsum = oracle.residual_rows(N, 42, x, np.arange(N))
+    tol = 2 * brute.gamma(N + 1) * (rowsum * np.max(np.abs(x)) + np.abs(b))
+    assert np.all(np.abs((rsum - b) - rr) <= tol)
+    assert abs(out4[0] - po[0]) <= np.max(tol)
+    assert out4[2] == po[2] and out4[3] == po[3]
+    assert abs(out4[1] - po[1]) <= brute.gamma(N) * po[1]
+    denom = U * (po[1] * po[2] + po[3]) * N
+    assert abs(r_k - ro) <= np.max(tol) / denom + 2 * brute.gamma(N) * ro
+    xp = x + 1e-2 * np.random.default_rng(N).uniform(-1, 1, N)
+    rp, _ = H.hplk_residual(42, N, xp)
+    rpo, _ = oracle.residual_seeded(N, 42, xp)
+    assert rp > 1e6 and rpo > 1e6
+    assert abs(rp - rpo) <= 1e-10 * rpo
+
+
+def test_residual_nonfinite_x_fails(H):
+    """A NaN or inf anywhere in x makes the device residual +inf (never
+    < 16; a max that drops NaN returned 0)."""
+    N = 512
+    with H.hpl_init(N, 64, 1, 1, 42) as ctx:
+        H.hpl_factor(ctx)
+        x = H.hpl_solve(ctx)
+    for bad in (np.nan, np.inf, -np.inf):
+        for k in (0, 300, N - 1):
+            xb = x.copy()
+            xb[k] = bad
+            r, out4 = H.hplk_residual(42, N, xb)
+            assert r == np.inf and not r < 16
+            assert oracle.residual_seeded(N, 42, xb)[0] >= 16 or \
+                np.isnan(oracle.residual_seeded(N, 42, xb)[0])
 
 
 # ------------------------------------------------------------------ end to end
@@ -266,69 +340,6 @@ def test_split_update_single_gpu_invariance(H):
     assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
 
 
-def test_store_l_invariance(H):
-    """Skipping the L21 write-back (option store_l=0: the solve needs only U
-    and y = L^-1 P b) leaves the pivots, x and the upper triangle bitwise
-    unchanged."""
-    def run(v):
-        with H.hpl_init(3000, 128, 1, 1, 23) as ctx:
-            H.hpl_set_option(ctx, "store_l", v)
-            H.hpl_factor(ctx)
-            LU = H.hpl_get_local(ctx)
-            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), np.triu(LU[:, :3000]), H.hpl_residual(ctx)
-    xa, pa, ua, ra = run(1)
-    xb, pb, ub, rb = run(0)
-    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and np.array_equal(ua, ub)
-    assert rb < 16
-
-
-@pytest.mark.parametrize("epi", [1, 2])
-def test_dgemm_epilogue_variants_bitwise(H, epi):
-    """The trailing DGEMM's RED (epi 1) and TMA reduce-add (epi 2) epilogues
-    compute C + (-acc) at the L2 — one rounding, bitwise C - acc — so a whole
-    solve gives the default epilogue's pivots and x bit for bit."""
-    def run(v):
-        with H.hpl_init(3000, 128, 1, 1, 29) as ctx:
-            H.hpl_set_option(ctx, "gemm_red", v)
-            try:
-                H.hpl_factor(ctx)
-                return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
-            finally:
-                H.hpl_set_option(ctx, "gemm_red", 0)   # process-wide knob
-    xa, pa, _ = run(0)
-    xb, pb, rb = run(epi)
-    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
-
-
-def test_stream_priority_invariance(H):
-    """The look-ahead stream one priority level below the RS/DTRSM stream
-    (option la_below_rs) only reorders concurrent kernels: bitwise equal."""
-    def run(v):
-        with H.hpl_init(4096, 256, 1, 1, 41) as ctx:
-            H.hpl_set_option(ctx, "la_below_rs", v)
-            H.hpl_factor(ctx)
-            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
-    xa, pa, _ = run(0)
-    xb, pb, rb = run(1)
-    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
-
-
-def test_trsm_pipe_invariance(H):
-    """DTRSM / DGEMM pipelined over column chunks (option trsm_pipe; active
-    while the trailing width >= 8192) moves no arithmetic between columns:
-    pivots and x bitwise equal to the one-launch schedule."""
-    def run(k):
-        with H.hpl_init(10240, 256, 1, 1, 19) as ctx:
-            H.hpl_set_option(ctx, "trsm_pipe", k)
-            H.hpl_factor(ctx)
-            return H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
-    xa, pa, ra = run(1)
-    xb, pb, rb = run(4)
-    xc, pc, rc = run(3)
-    assert np.array_equal(pa, pb) and np.array_equal(xa, xb) and rb < 16
-    assert np.array_equal(pa, pc) and np.array_equal(xa, xc) and rc < 16
-
-
 @pytest.mark.parametrize("opts", [{"leaf_warp": 148, "leaf_hide_ms": 0},
                                   {"leaf_warp": 7, "leaf_hide_ms": 0},
                                   {"leaf_ctas": 3}, {"leaf_ctas": 0}])
@@ -347,6 +358,19 @@ def test_leaf_grid_invariance(H, opts):
     o = oracle.run(3000, 17)
     assert np.array_equal(pb, o["ipiv"]) and np.array_equal(pa, pb)
     assert np.array_equal(xa, xb) and rb < 16
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_gemm_cfg_end_to_end(H, cfg):
+    """Every DGEMM tile config (option gemm_cfg) through hpl_factor: the
+    oracle's pivots and x within 1e-9."""
+    with H.hpl_init(2048, 128, 1, 1, 43) as ctx:
+        H.hpl_set_option(ctx, "gemm_cfg", cfg)
+        H.hpl_factor(ctx)
+        x, ipiv, r = H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_residual(ctx)
+    o = oracle.run(2048, 43)
+    assert np.array_equal(ipiv, o["ipiv"]) and r < 16
+    assert np.max(np.abs(x - o["x"])) / np.max(np.abs(o["x"])) <= 1e-9
 
 
 def test_hpl_c1_vs_oracle(H):
@@ -378,7 +402,8 @@ def test_singular_reported(H):
 
 
 def test_load_local_matches_oracle_solve(H):
-    """Hand-made system through hpl_load_local (the e2e host path)."""
+    """Hand-made system through hpl_load_local (the e2e host path); the
+    seeded residual does not apply to it (HPL_ERR_STATE, not a wrong number)."""
     N = 300
     rng = np.random.default_rng(3)
     Ab = rng.uniform(-0.5, 0.5, (N, N + 1))
@@ -387,6 +412,14 @@ def test_load_local_matches_oracle_solve(H):
         H.hpl_factor(ctx)
         x = H.hpl_solve(ctx)
         ipiv = H.hpl_get_ipiv(ctx)
+        with pytest.raises(H.HplError) as ei:
+            H.hpl_residual(ctx)
+        assert ei.value.status == 2
+        # back to the seeded system: the residual is available again
+        H.hpl_regenerate(ctx)
+        H.hpl_factor(ctx)
+        H.hpl_solve(ctx)
+        assert H.hpl_residual(ctx) < 16
     LU, ipo, _ = oracle.getrf(Ab[:, :N])
     xo = oracle.getrs(LU, ipo, Ab[:, N])
     assert np.array_equal(ipiv, ipo)
@@ -413,3 +446,11 @@ def test_hpl_full_size_c2_sampled(H):
     bn = max(abs(oracle.gen_entry(seed, N, i, N)) for i in rows)
     sampled = np.max(np.abs(rr)) / (U * (np.max(rowsum) * np.max(np.abs(x)) + bn) * N)
     assert sampled < 16.0
+    # the device residual kernels on the same x: the ABI value bitwise, and
+    # the sampled rows elementwise vs the oracle within the dot-product bound
+    r_k, out4, rsum, asum = H.hplk_residual(seed, N, x, want_rows=True)
+    assert r_k == r
+    b = np.array([oracle.gen_entry(seed, N, i, N) for i in rows])
+    tol = 2 * brute.gamma(N + 1) * (rowsum * np.max(np.abs(x)) + np.abs(b))
+    assert np.all(np.abs((rsum[rows] - b) - rr) <= tol)
+    assert np.all(np.abs(asum[rows] - rowsum) <= brute.gamma(N) * rowsum)
