@@ -85,7 +85,8 @@ def parse():
     ap.add_argument("--block", dest="nb", type=int, default=512)
     ap.add_argument("--grid", default="", help="PxQ process grid (default: BASELINE.json's grid)")
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--cpu-n", type=int, default=4096)
+    ap.add_argument("--cpu-n", type=int, default=8192, help="oracle sample size (C1)")
+    ap.add_argument("--ref-n", type=int, default=4096, help="--impl reference: oracle N per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -173,16 +174,16 @@ def run_reference(a, rank, world):
     if rank != 0:
         return 0
     for _ in range(a.warmup):
-        cpu_baseline(min(a.cpu_n, 1024), a.seed)
+        cpu_baseline(min(a.ref_n, 1024), a.seed)
     times = []
     for _ in range(a.steps):
-        tf, dt, thr, r = cpu_baseline(a.cpu_n, a.seed)
+        tf, dt, thr, r = cpu_baseline(a.ref_n, a.seed)
         if not r < 16.0:
             print(json.dumps({"impl": "reference", "error": f"oracle residual {r}"}))
             return 1
         times.append(dt)
     T = sum(times)
-    value = a.steps * hpl_flops(a.cpu_n) / T / 1e12
+    value = a.steps * hpl_flops(a.ref_n) / T / 1e12
     N, NB, P, Q = workload(a, world)
     line = {
         "impl": "reference",
@@ -190,10 +191,10 @@ def run_reference(a, rank, world):
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * T / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded HPL generator, DESIGN.md reading A6)",
-        "config": {"workload": f"HPL N={N} NB={NB} {P}x{Q} grid", "sample": f"full solve at N={a.cpu_n}",
+        "config": {"workload": f"HPL N={N} NB={NB} {P}x{Q} grid", "sample": f"full solve at N={a.ref_n}",
                    "N": N, "NB": NB, "grid": f"{P}x{Q}", "l2": "inputs > L2"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
-                         "sample": f"oracle GEPP+solves, full solve at N={a.cpu_n} "
+                         "sample": f"oracle GEPP+solves, full solve at N={a.ref_n} "
                                    f"(bounded sample of the N={N} workload), {cpu_model()}"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -246,25 +247,31 @@ def main():
 
     fl = hpl_flops(N)
     resids = []
+    xs = []
 
-    def step():
+    def step(want_x=False):
         H.hpl_regenerate(ctx)
         barrier()
         H.hpl_factor(ctx)
-        H.hpl_solve(ctx, want_x=False)
+        x = H.hpl_solve(ctx, want_x=want_x)
         barrier()
         t = H.hpl_last_timing(ctx)
+        t["phases"] = H.hpl_phase_stats(ctx)
         r = H.hpl_residual(ctx)
         if not r < 16.0:
             raise SystemExit(f"rank {rank}: HPL residual {r} >= 16 (FAILED)")
         resids.append(r)
+        if want_x:
+            xs.append(x)
         return t
 
     for _ in range(a.warmup):
         step()
     clocks = Clocks(local)
     clocks.start()
-    tims = [step() for _ in range(a.steps)]
+    # the last timed step also returns x (a 8*N-byte D2H inside its solve):
+    # the e2e solve of the same system must reproduce it
+    tims = [step(want_x=(k == a.steps - 1)) for k in range(a.steps)]
     ck = clocks.stop()
     dev_ms = sum(t["factor_ms"] + t["solve_ms"] for t in tims)
     dev_ms = allmax(dev_ms)
@@ -274,6 +281,25 @@ def main():
     launches = sum(t["launches"] for t in tims) // max(1, a.steps)
     value = a.steps * fl / (dev_ms * 1e-3) / 1e12   # one P x Q system over all GPUs
     dg_tf = dg_fl / (dg_ms * 1e-3) / 1e12 if dg_ms > 0 else None
+    # rooflines of the non-DGEMM phases (summed CUDA-event times over the
+    # timed steps, algorithmic bytes / flop from the library: hpl_phase_stats)
+    ph = {k: sum(t["phases"][k] for t in tims) for k in tims[0]["phases"]}
+    phases = {
+        "laswp": {"kernel": "laswp_gs_kernel (P=1) / rs_gather_peer + rs_scatter (P>1), rest columns",
+                  "bytes": ph["laswp_bytes"] / a.steps, "ms": ph["laswp_ms"] / a.steps,
+                  "GBps": ph["laswp_bytes"] / (ph["laswp_ms"] * 1e-3) / 1e9 if ph["laswp_ms"] > 0 else None,
+                  "bound": "hbm"},
+        "dtrsm": {"kernel": "dgemm_tma_kernel ASSIGN a_lower (L11^-1 U), rest columns",
+                  "flop": ph["trsm_flop"] / a.steps, "ms": ph["trsm_ms"] / a.steps,
+                  "TFLOPs": ph["trsm_flop"] / (ph["trsm_ms"] * 1e-3) / 1e12 if ph["trsm_ms"] > 0 else None,
+                  "bound": "tensor"},
+        "fact": {"kernel": "panel FACT (recursive, device leaf), summed over panels",
+                 "ms": ph["fact_ms"] / a.steps, "bound": "latency"},
+        "solve": {"kernel": "bs_partial + bs_diag", "bytes": ph["solve_bytes"] / a.steps,
+                  "ms": ph["solve_ms"] / a.steps,
+                  "GBps": ph["solve_bytes"] / (ph["solve_ms"] * 1e-3) / 1e9 if ph["solve_ms"] > 0 else None,
+                  "bound": "hbm"},
+    }
 
     # ---- end to end through the public API with host buffers (pinned)
     e2e = None
@@ -301,10 +327,14 @@ def main():
             ctx.check(H.hpl.lib.hpl_solve(ctx.h, H.hpl.ptr(xh)))
             barrier()
             dt = allmax(time.perf_counter() - t0)
-            r = H.hpl_residual(ctx)
-            if not r < 16.0:
-                raise SystemExit(f"e2e residual {r} >= 16")
-            e2e = {"value": fl / dt / 1e12, "unit": "TFLOP/s",
+            # the loaded system is the seeded one (read back after
+            # hpl_regenerate): its x must be the verified x of the last
+            # timed step (deterministic schedule, bitwise)
+            same = bool(np.array_equal(xh, xs[-1]))
+            rel = float(np.max(np.abs(xh - xs[-1])) / np.max(np.abs(xs[-1])))
+            if not rel <= 1e-12:
+                raise SystemExit(f"e2e x differs from the device-path x: {rel}")
+            e2e = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "x_equal_device_path": same,
                    "h2d_bytes_per_step": int(rows * cols * 8) * world,
                    "d2h_bytes_per_step": int(N * 8) * world, "pinned": pinned, "s": dt}
             if pinned:
@@ -313,10 +343,17 @@ def main():
 
     cpu = None
     if rank == 0 and not a.no_cpu:
-        tf, dt, thr, rr = cpu_baseline(a.cpu_n, a.seed)
-        cpu = {"value": tf, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
-               "sample": f"oracle GEPP+solves, full solve at N={a.cpu_n} ({dt:.1f} s; bounded "
-                         f"sample of the N={N} workload), {cpu_model()}", "resid": rr}
+        # BASELINE.json configs[0] (C0) and configs[1] (C1): full oracle
+        # solves; C1's rate is the reported baseline
+        per = {}
+        for n_cpu in (256, a.cpu_n):
+            tf, dt, thr, rr = cpu_baseline(n_cpu, a.seed)
+            per[f"N={n_cpu}"] = {"TFLOPs": tf, "s": dt, "resid": rr}
+        cpu = {"value": per[f"N={a.cpu_n}"]["TFLOPs"], "unit": "TFLOP/s", "cores": thr,
+               "kind": "oracle",
+               "sample": f"oracle GEPP+solves, full solves at N=256 (C0) and N={a.cpu_n} (C1; "
+                         f"the value), bounded samples of the N={N} workload, {cpu_model()}",
+               "per_config": per}
 
     traffic, traffic_note = None, None
     tf_path = os.path.join(ROOT, "profiles", "dgemm_traffic.json")
@@ -357,6 +394,7 @@ def main():
                                     ".json has no FP64 entry)",
                      "peak_measured_dmma": peak_meas,
                      "cublas_dgemm_8192": cublas_tf},
+        "phases": phases,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
