@@ -1,7 +1,9 @@
-"""Multi-GPU parity (-m gpu, needs >= 2 visible GPUs): 1 x Q grids over NCCL,
-launched with torchrun, compared with the CPU oracle (identical pivots, x
-within 1e-9, residual < 16, x replicated on every rank) — SPEC.md l.363
-cross-grid consistency."""
+"""Multi-GPU parity (-m gpu, needs >= 2 visible GPUs): P x Q grids with one
+process per GPU (torchrun), the exchanges over CUDA-IPC peer memory (NCCL
+only carries the handle exchange, and the coll_nccl / rs_peer=0 / lb_peer=0
+variants), compared with the CPU oracle (identical pivots, x within 1e-9,
+residual < 16, x replicated on every rank) — SPEC.md l.363 cross-grid
+consistency.  The same data path runs on one GPU in tests/test_loopback.py."""
 import json
 import os
 import socket
@@ -101,7 +103,7 @@ def test_8gpu_grids_vs_oracle(N, NB, P, Q):
 
 def test_split_update_schedule_invariance():
     """split update on/off gives the identical pivot sequence
-    (P = 2, RS across GPUs; the split update is the default there)."""
+    (P = 2, the RS crossing GPUs; split is off by default)."""
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     a = _run(2, 3072, 128, 2, 1, ("--opt=split=0",))
@@ -122,37 +124,36 @@ def test_2x1_warp_leaf(opts):
 
 @pytest.mark.parametrize("P,Q,split", [(2, 1, 0), (2, 1, 30), (1, 2, 0), (2, 2, 0)])
 def test_peer_exchange_vs_nccl(P, Q, split):
-    """The RS and LBCAST over NVLink peer memory (defaults: rs_peer, lb_peer)
-    and their NCCL versions (all-reduce + broadcast RS, broadcast LBCAST) both
-    give the oracle's pivots and x, with and without the split update."""
+    """The RS and LBCAST over NVLink peer memory (defaults: rs_peer=1,
+    lb_peer=1) and their NCCL versions (all-reduce + broadcast RS, broadcast
+    LBCAST, every collective over NCCL: coll_nccl=1) both give the oracle's
+    pivots and x, with and without the split update."""
     if _ngpu() < P * Q:
         pytest.skip(f"needs {P * Q} GPUs")
     for v in (1, 0):
         out = _run(P * Q, 3000, 128, P, Q,
-                   (f"--opt=rs_peer={v}", f"--opt=lb_peer={v}", f"--opt=split={split}"))
+                   (f"--opt=rs_peer={v}", f"--opt=lb_peer={v}", f"--opt=coll_nccl={1 - v}",
+                    f"--opt=split={split}"))
         assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16, (v, out)
 
 
-def test_peer_exchange_two_factorizations():
-    """Flags are monotonic across factorizations of one context (hpl_regenerate
-    then a second hpl_factor): the second solve still matches the oracle."""
-    if _ngpu() < 4:
-        pytest.skip("needs 4 GPUs")
-    out = _run(4, 2048, 64, 2, 2, ("--repeat", "2"))
-    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16
-
-
-@pytest.mark.parametrize("P,Q", [(2, 1), (2, 2)])
-def test_gathered_fact_vs_distributed(P, Q):
-    """P > 1 panel FACT two ways: the distributed leaf (one NVLink pivot
-    exchange per column, fact_gather=0) and the gathered FACT (every process
-    of the column factors the combined panel; the default for small panels
-    whose trailing update is short).  Both give the oracle's pivots and x within 1e-9, and
-    the same x (same arithmetic), also with a threshold that switches mode
-    mid-run."""
-    if _ngpu() < P * Q:
-        pytest.skip(f"needs {P * Q} GPUs")
-    outs = [_run(P * Q, 3000, 128, P, Q, (f"--opt=fact_gather={g}",)) for g in (0, 1 << 20, 1500)]
-    for o in outs:
-        assert o["ipiv_equal"] and o["x_rel"] <= 1e-9 and o["resid"] < 16, o
-    assert outs[0]["x_rel"] == outs[1]["x_rel"] == outs[2]["x_rel"]
+def test_rank_death_gives_peer_error():
+    """SPEC.md l.191 / l.360: rank 1 exits 300 ms into hpl_factor; rank 0's
+    bounded peer waits end its call with HPL_ERR_PEER instead of a hang.
+    (Two plain processes, not torchrun: its agent would kill rank 0 too.)"""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    port = str(_port())
+    procs = []
+    for rank in (0, 1):
+        env = dict(os.environ, PYTHONPATH=ROOT, RANK=str(rank), LOCAL_RANK=str(rank),
+                   WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+        cmd = [sys.executable, os.path.join(ROOT, "tools", "dist_hpl.py"), "65536", "512", "1",
+               "2", "42", "--die", "1:300", "--timeout-ms", "5000"]
+        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                      text=True, env=env))
+    outs = [p.communicate(timeout=300) for p in procs]
+    lines = [json.loads(l) for l in outs[0][0].splitlines() if l.startswith("{")]
+    assert procs[1].returncode == 3, outs[1]
+    assert lines and lines[0]["rank"] == 0 and lines[0]["status"] == 7, outs[0]
+    assert lines[0]["wall_s"] < 120

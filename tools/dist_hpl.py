@@ -2,6 +2,7 @@
 
     torchrun --nproc-per-node Q --master-addr 127.0.0.1 --master-port PORT \\
         tools/dist_hpl.py N NB P Q [seed] [--oracle] [--la 0|1] [--repeat K] [--opt=k=v]
+        [--die RANK:MS] [--timeout-ms T]
 
 rank 0 creates the NCCL unique id (hpl_get_unique_id); it travels to the other
 ranks over a gloo process group; every rank then calls hpl_init_dist.  With
@@ -42,6 +43,26 @@ def main():
     for kv in [a for a in sys.argv[1:] if a.startswith("--opt=")]:
         k, v = kv[len("--opt="):].split("=")
         H.hpl_set_option(ctx, k, int(v))
+    if "--timeout-ms" in sys.argv:
+        H.hpl_set_option(ctx, "peer_timeout_ms", int(sys.argv[sys.argv.index("--timeout-ms") + 1]))
+    if "--die" in sys.argv:
+        # failure detection: rank R exits MS ms into
+        # hpl_factor; every other rank must get HPL_ERR_PEER, not hang
+        die_rank, die_ms = (int(v) for v in sys.argv[sys.argv.index("--die") + 1].split(":"))
+        if rank == die_rank:
+            import threading
+            threading.Timer(die_ms / 1000.0, lambda: os._exit(3)).start()
+        dist.barrier()
+        t0 = time.perf_counter()
+        try:
+            H.hpl_factor(ctx)
+            H.hpl_solve(ctx)
+            status, msg = 0, ""
+        except H.HplError as e:
+            status, msg = e.status, str(e)
+        print(json.dumps(dict(rank=rank, status=status, msg=msg[:300],
+                              wall_s=time.perf_counter() - t0)), flush=True)
+        os._exit(0 if status == 7 else 1)
     timeline = "--timeline" in sys.argv
     repeat = int(sys.argv[sys.argv.index("--repeat") + 1]) if "--repeat" in sys.argv else 1
     for _ in range(repeat - 1):      # earlier factorizations of the same context
