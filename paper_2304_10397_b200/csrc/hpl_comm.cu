@@ -89,7 +89,8 @@ hpl_status alloc_ctx(hpl_ctx *c)
     if (!M((void **)&c->U2, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
     if (!M((void **)&c->scratch, sizeof(double) * round_up(NBs, 16) * NBs)) return HPL_ERR_OOM;
     if (!M((void **)&c->x, sizeof(double) * (size_t)c->N)) return HPL_ERR_OOM;
-    if (!M((void **)&c->tbuf, sizeof(double) * 16 * NBs)) return HPL_ERR_OOM;
+    // back-solve partial sums: 2 parities x (<= 16 far shares + 1 near share) x NB
+    if (!M((void **)&c->tbuf, sizeof(double) * 2 * 17 * NBs)) return HPL_ERR_OOM;
     if (!M((void **)&c->out4, sizeof(double) * 4)) return HPL_ERR_OOM;
     if (cudaMallocHost((void **)&c->hstage, sizeof(double) * (size_t)std::max<int64_t>(c->N, 16)) !=
         cudaSuccess) {

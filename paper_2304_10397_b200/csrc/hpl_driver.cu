@@ -595,36 +595,90 @@ hpl_status hpl_solve(hpl_ctx *c, double *x_host)
     CK(c, cudaEventRecord(c->ev_t[1], c->s_la));
     trace(c, "solve event recorded");
     {
-        // Distributed block back substitution.  Block row bb lives on process
-        // row rb = bb mod P: its Q processes form the partial sums over their
-        // local columns (all-reduce over the process row), the owner of the
-        // diagonal block (rb, bb mod Q) solves it, and x_b is broadcast to
-        // every rank so x stays replicated.
-        const int64_t N = c->N, nblk = cdiv(N, c->NB);
-        const int ycol = (int)((N / c->NB) % c->Q);            // owner of global column N
+        // Distributed block back substitution U x = y,
+        // bottom block first, with a look-ahead.  Block row bb lives on
+        // process row rb = bb mod P; its partial sums over the local columns
+        // are split into FAR (column blocks >= bb+2, whose x is known one step
+        // early) and NEAR (column block bb+1).  The far sums of block bb-2 run
+        // on S_tr while S_la carries the critical chain of block bb: near
+        // sums -> all-reduce over the process row -> diagonal solve on the
+        // owner of block (bb, bb) -> broadcast of x_bb to every rank (x stays
+        // replicated).  Partial buffers alternate by the parity of bb.  The far
+        // sums run on the LOW-priority S_tr: the chain's kernels (the 16-CTA
+        // cluster diagonal solve needs 16 free SMs of one GPC) get SMs first.
+        const int64_t N = c->N, NB = c->NB, nblk = cdiv(N, NB);
+        const int ycol = (int)((N / NB) % c->Q);            // owner of global column N
         const int64_t lcy = c->mycol == ycol ? lcols_before(c, N) : -1;
         const int64_t lcN = lcols_before(c, N);
+        auto geom = [&](int64_t bb, int64_t *r0, int64_t *r1, int *nb, int64_t *farlo) {
+            *r0 = bb * NB;
+            *r1 = std::min<int64_t>(N, *r0 + NB);
+            *nb = (int)(*r1 - *r0);
+            *farlo = std::min<int64_t>(N, *r1 + NB);
+        };
+        // split count of the far sums: global sizes only, so the all-reduce
+        // lines up on every rank of the process row
+        auto sfar = [&](int64_t bb) {
+            int64_t r0, r1, farlo;
+            int nb;
+            geom(bb, &r0, &r1, &nb, &farlo);
+            return bs_splits(nb, 0, cdiv(cdiv(N - farlo, NB), c->Q) * NB, (int)NB);
+        };
+        auto tb = [&](int64_t bb) { return c->tbuf + (bb & 1) * (int64_t)17 * NB; };
+        cudaEvent_t ev_far[2] = {c->ev_rsR, c->ev_rsL}, ev_x = c->ev_dgR;
+        auto far = [&](int64_t bb) -> hpl_status {
+            if (bb < 0) return HPL_OK;
+            if (c->myrow == (int)(bb % c->P)) {
+                int64_t r0, r1, farlo;
+                int nb;
+                geom(bb, &r0, &r1, &nb, &farlo);
+                CK(c, bs_partial(c->s_tr, nb, c->A + lrows_before(c, r0) * c->lda, c->lda,
+                                 lcols_before(c, farlo), lcN, (int)NB, c->Q, c->mycol, c->x, lcy,
+                                 tb(bb), sfar(bb)));
+            }
+            CK(c, cudaEventRecord(ev_far[bb & 1], c->s_tr));
+            return HPL_OK;
+        };
+        CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_t[1], 0));
+        ST(far(nblk - 1));
+        ST(far(nblk - 2));
         for (int64_t bb = nblk - 1; bb >= 0; --bb) {
-            const int64_t r0 = bb * c->NB, r1 = std::min<int64_t>(N, r0 + c->NB);
-            const int nb = (int)(r1 - r0);
+            int64_t r0, r1, farlo;
+            int nb;
+            geom(bb, &r0, &r1, &nb, &farlo);
             const int rb = (int)(bb % c->P), qb = (int)(bb % c->Q);
             if (c->myrow == rb) {
                 if (bb == nblk - 1) trace(c, "solve first partial");
                 const int64_t lr0 = lrows_before(c, r0);
-                // every rank of the process row uses the same split count
-                // (a function of the global sizes) so the all-reduce lines up
-                const int S = bs_splits(nb, 0, cdiv(cdiv(N - r1, c->NB), c->Q) * c->NB, c->NB);
-                CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda,
-                                 lcols_before(c, r1), lcN, c->NB, c->Q, c->mycol, c->x,
-                                 lcy, c->tbuf, S));
-                ST(coll_allreduce(c, G_ROW, c->tbuf, (int64_t)S * nb, COLL_SUM, c->s_la));
-                if (c->mycol == qb)
-                    CK(c, bs_diag(c->s_la, nb, c->A + lr0 * c->lda + lcols_before(c, r0), c->lda,
-                                  c->tbuf, S, c->x + r0));
+                const int S = sfar(bb);
+                double *Ubb = c->A + lr0 * c->lda + lcols_before(c, r0);
+                if (c->Q == 1 && bs_diag_folds_near(nb)) {
+                    // one process column: no row reduction, the near sums go into
+                    // the diagonal solve (one launch per block on the chain)
+                    CK(c, cudaStreamWaitEvent(c->s_la, ev_far[bb & 1], 0));
+                    CK(c, bs_diag(c->s_la, nb, Ubb, c->lda, tb(bb), S, c->x + r0,
+                                  (int)(farlo - r1), c->x + r1));
+                } else {
+                    CK(c, bs_partial(c->s_la, nb, c->A + lr0 * c->lda, c->lda, lcols_before(c, r1),
+                                     lcols_before(c, farlo), (int)NB, c->Q, c->mycol, c->x, -1,
+                                     tb(bb) + (int64_t)S * nb, 1));
+                    CK(c, cudaStreamWaitEvent(c->s_la, ev_far[bb & 1], 0));
+                    ST(coll_allreduce(c, G_ROW, tb(bb), (int64_t)(S + 1) * nb, COLL_SUM, c->s_la));
+                    if (c->mycol == qb)
+                        CK(c, bs_diag(c->s_la, nb, Ubb, c->lda, tb(bb), S + 1, c->x + r0));
+                }
+            } else {
+                CK(c, cudaStreamWaitEvent(c->s_la, ev_far[bb & 1], 0));
             }
             ST(coll_bcast(c, G_WORLD, c->x + r0, sizeof(double) * nb, rb + qb * c->P, c->s_la));
             if (bb >= nblk - 2) trace(c, "solve block enqueued", bb);
+            // x_bb is known everywhere: the far sums of block bb-2 may start
+            CK(c, cudaEventRecord(ev_x, c->s_la));
+            CK(c, cudaStreamWaitEvent(c->s_tr, ev_x, 0));
+            ST(far(bb - 2));
         }
+        CK(c, cudaEventRecord(ev_x, c->s_tr));
+        CK(c, cudaStreamWaitEvent(c->s_la, ev_x, 0));
     }
     if (x_host)
         CK(c, cudaMemcpyAsync(c->hstage, c->x, sizeof(double) * c->N, cudaMemcpyDeviceToHost,

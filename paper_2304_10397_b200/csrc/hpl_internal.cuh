@@ -335,9 +335,13 @@ int bs_splits(int nb, int64_t lc_lo, int64_t lc_hi, int NB);
 cudaError_t bs_partial(cudaStream_t st, int nb, const double *Urows, int64_t ldu, int64_t lc_lo,
                        int64_t lc_hi, int NB, int Q, int mycol, const double *x, int64_t lcy,
                        double *partial, int S);
-// xb = U_bb^{-1} (-sum_s partial[s])
+// xb = U_bb^{-1} (-sum_s partial[s] - U_near x_near): nnear > 0 folds the
+// near sums (the next nnear columns of the block's rows times xnear) into the
+// solve; only when bs_diag_folds_near(nb) (the cluster solve is available).
 cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
-                    const double *partial, int S, double *xb);
+                    const double *partial, int S, double *xb, int nnear = 0,
+                    const double *xnear = nullptr);
+bool bs_diag_folds_near(int nb);
 // Residual of the seeded system: per-rank partial sums (local rows x local
 // columns), then (after the caller's all-reduce over the process row) the
 // norms into out4 = {rinf, anorm, xnorm, bnorm} (max over local rows; a

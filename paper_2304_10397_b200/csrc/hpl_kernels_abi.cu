@@ -143,7 +143,7 @@ int hplk_back_solve(int64_t N, int32_t NB, const double *U, int64_t ldu, const d
     Dev dU, dX, dT;
     KT(dU.alloc(sizeof(double) * dl * N));
     KT(dX.alloc(sizeof(double) * N));
-    KT(dT.alloc(sizeof(double) * 16 * NB));
+    KT(dT.alloc(sizeof(double) * 2 * 17 * NB));
     KT(cudaMemcpy2D(dU.p, dl * 8, U, ldu * 8, N * 8, N, cudaMemcpyHostToDevice));
     // y goes into column N (the layout hpl_solve sees)
     KT(cudaMemcpy2D(dU.as<double>() + N, dl * 8, y, 8, 8, N, cudaMemcpyHostToDevice));

@@ -46,6 +46,7 @@ struct GemmParams {
     int prefetch_c;
     unsigned zero;       // always 0; opaque to the compiler (see release below)
     int ntiles;          // tiles_m * tiles_n; CTA b owns tiles b, b + gridDim.x, ...
+    int pair_lower;      // a_lower with even tiles_m: CTA b owns m-tiles i and tiles_m-1-i
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -154,12 +155,24 @@ dgemm_tma_kernel(const GemmParams p, const __grid_constant__ ParamPad<SLOT> pad,
     // one continuous TMA/mbarrier pipeline (the next tile's stages load while
     // the consumers run the current tile's epilogue)
     auto tile_coords = [&](int tile, int &m0, int &n0, int &nk) {
-        const int group_sz = GROUP_M * p.tiles_n;
-        const int gid = tile / group_sz;
-        const int first_m = gid * GROUP_M;
-        const int gm = min(p.tiles_m - first_m, GROUP_M);
-        const int pm = first_m + (tile % group_sz) % gm;
-        const int pn = (tile % group_sz) / gm;
+        int pm, pn;
+        if (p.pair_lower) {
+            // triangular A (the DTRSM's L11^{-1}): m-tile i needs k < 64(i+1),
+            // so tile i and its partner tiles_m-1-i together always cost
+            // tiles_m+1 tiles of k — every CTA gets the same work
+            const int half = p.tiles_m >> 1, G = half * p.tiles_n;
+            const bool second = tile >= G;
+            const int t = second ? tile - G : tile;
+            pn = t / half;
+            pm = second ? p.tiles_m - 1 - t % half : t % half;
+        } else {
+            const int group_sz = GROUP_M * p.tiles_n;
+            const int gid = tile / group_sz;
+            const int first_m = gid * GROUP_M;
+            const int gm = min(p.tiles_m - first_m, GROUP_M);
+            pm = first_m + (tile % group_sz) % gm;
+            pn = (tile % group_sz) / gm;
+        }
         m0 = pm * C::BM;
         n0 = pn * C::BN;
         int k_end = p.k;
@@ -390,7 +403,8 @@ cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMa
     });
     HPL_CUDA_TRY(attr_err);
     ParamPad<SLOT> pad{};
-    dgemm_tma_kernel<C, SLOT><<<(unsigned)p.ntiles, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
+    const unsigned grid = (unsigned)(p.pair_lower ? p.ntiles / 2 : p.ntiles);
+    dgemm_tma_kernel<C, SLOT><<<grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
     count_launch();
     return cudaGetLastError();
 }
@@ -401,7 +415,8 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
 {
     p.tiles_m = (int)cdiv(p.m, C::BM);
     p.tiles_n = (int)cdiv(p.n, C::BN);
-    p.ntiles = p.tiles_m * p.tiles_n;     // one tile per CTA
+    p.ntiles = p.tiles_m * p.tiles_n;     // one tile per CTA (two when pair_lower)
+    p.pair_lower = p.a_lower && p.tiles_m >= 2 && (p.tiles_m & 1) == 0;
     switch (slot) {
     case SLOT_LOOKAHEAD: return launch_slot<C, SLOT_LOOKAHEAD>(st, ma, mb, p);
     case SLOT_FACT: return launch_slot<C, SLOT_FACT>(st, ma, mb, p);

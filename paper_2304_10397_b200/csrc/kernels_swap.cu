@@ -74,40 +74,69 @@ __global__ void pivot_plan_kernel(int jb, long long r0, const int64_t *__restric
 
 constexpr int LS_COLS = 64;      // columns per CTA (one warp covers 64 doubles with 16B lanes)
 constexpr int LS_WARPS = 8;
+constexpr int LS_UNROLL = 4;     // row copies in flight per warp (HBM latency x bandwidth)
+constexpr int LS_MAXJB = 1024;
 
+// One pass over columns [c0, c1) of the row swaps of one panel: every CTA
+// first stages the plan (src rows, displaced pairs) in shared memory, then
+// each warp moves LS_UNROLL rows at a time with 16-byte lanes (all loads of
+// a group issued before its stores).  Phase 1 gathers the block's final
+// rows into U; after a CTA barrier (every read of a displaced row precedes
+// its overwrite) phase 2 writes the displaced rows.
 __global__ void __launch_bounds__(LS_WARPS * 32)
 laswp_gs_kernel(int jb, const int64_t *__restrict__ src, const int64_t *__restrict__ disp,
                 const int *__restrict__ ndisp, double *A, long long lda, long long c0,
                 long long c1, double *U, long long ldu, int vec)
 {
+    __shared__ long long s_src[LS_MAXJB];
+    __shared__ long long s_dd[LS_MAXJB], s_ds[LS_MAXJB];
+    const int nd = *ndisp;
+    for (int k = threadIdx.x; k < jb; k += blockDim.x) s_src[k] = src[k];
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+        s_dd[d] = disp[2 * d];
+        s_ds[d] = disp[2 * d + 1];
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long cb = c0 + (long long)blockIdx.x * LS_COLS;  // first column of this CTA
     const long long col = cb + 2 * lane;
     const bool has0 = col < c1, has1 = col + 1 < c1;
+    auto move = [&](int total, auto srow, auto drow) {
+        for (int k0 = warp * LS_UNROLL; k0 < total; k0 += LS_WARPS * LS_UNROLL) {
+            if (vec && has1) {
+                double2 v[LS_UNROLL];
+#pragma unroll
+                for (int u = 0; u < LS_UNROLL; ++u)
+                    if (k0 + u < total)
+                        v[u] = *reinterpret_cast<const double2 *>(srow(k0 + u));
+#pragma unroll
+                for (int u = 0; u < LS_UNROLL; ++u)
+                    if (k0 + u < total) *reinterpret_cast<double2 *>(drow(k0 + u)) = v[u];
+            } else {
+                double v0[LS_UNROLL], v1[LS_UNROLL];
+#pragma unroll
+                for (int u = 0; u < LS_UNROLL; ++u)
+                    if (k0 + u < total) {
+                        v0[u] = has0 ? srow(k0 + u)[0] : 0.0;
+                        v1[u] = has1 ? srow(k0 + u)[1] : 0.0;
+                    }
+#pragma unroll
+                for (int u = 0; u < LS_UNROLL; ++u)
+                    if (k0 + u < total) {
+                        if (has0) drow(k0 + u)[0] = v0[u];
+                        if (has1) drow(k0 + u)[1] = v1[u];
+                    }
+            }
+        }
+    };
+    // (the accessors return this lane's element: A column col, U column col - c0)
     // phase 1: gather the block's final rows into U
-    for (int k = warp; k < jb; k += LS_WARPS) {
-        const double *s = A + src[k] * lda + col;
-        double *d = U + (long long)k * ldu + (col - c0);
-        if (vec && has1) {
-            *reinterpret_cast<double2 *>(d) = *reinterpret_cast<const double2 *>(s);
-        } else {
-            if (has0) d[0] = s[0];
-            if (has1) d[1] = s[1];
-        }
-    }
-    __syncthreads();  // every read of a displaced row precedes its overwrite
+    move(jb, [&](int k) -> const double * { return A + s_src[k] * lda + col; },
+         [&](int k) -> double * { return U + (long long)k * ldu + (col - c0); });
+    __syncthreads();
     // phase 2: displaced rows receive original block rows
-    const int nd = *ndisp;
-    for (int d = warp; d < nd; d += LS_WARPS) {
-        const double *s = A + disp[2 * d + 1] * lda + col;
-        double *t = A + disp[2 * d] * lda + col;
-        if (vec && has1) {
-            *reinterpret_cast<double2 *>(t) = *reinterpret_cast<const double2 *>(s);
-        } else {
-            if (has0) t[0] = s[0];
-            if (has1) t[1] = s[1];
-        }
-    }
+    move(nd, [&](int d) -> const double * { return A + s_ds[d] * lda + col; },
+         [&](int d) -> double * { return A + s_dd[d] * lda + col; });
 }
 
 // ---- P > 1: the row swaps cross process rows (RS over the column communicator)
@@ -335,6 +364,7 @@ cudaError_t laswp_gather_scatter(cudaStream_t st, int64_t jb, const int64_t *src
                                  int64_t c0, int64_t c1, double *U, int64_t ldu)
 {
     if (jb <= 0 || c1 <= c0) return cudaSuccess;
+    if (jb > LS_MAXJB) return cudaErrorInvalidValue;
     const int vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda & 1) == 0 &&
                      (c0 & 1) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&
                      (ldu & 1) == 0)
