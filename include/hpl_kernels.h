@@ -58,6 +58,21 @@ int hplk_panel_fact(int64_t m, int64_t nb, double *P, int64_t ldp, int64_t *ipiv
 int hplk_laswp(int64_t rows, int64_t cols, double *A, int64_t lda, int64_t j0, int64_t jb,
                const int64_t *ipiv, int64_t c0, int64_t c1, double *U, int64_t ldu);
 
+/* a2+a3 RS (P > 1 row swaps across process rows, PAPER.md l.9 / l.60): the
+ * global rows x cols matrix A (row-major lda) is distributed over P process
+ * rows block-cyclically (NB-row blocks, block I on process row I mod P), each
+ * process row's local rows in their own device buffer — the layout of P
+ * ranks, here in one process.  Applies the swaps (j0+k) <-> ipiv[k] (global
+ * rows, k < jb, in order) to all columns with the kernels hpl_factor uses:
+ * rs_gather_peer on every process row (U = the block's final rows, read from
+ * their owners' buffers; W = the original block rows its displaced rows
+ * receive), then rs_scatter.  U (jb x cols, row-major ldu) receives process
+ * row 0's gathered rows (every process row's U is checked equal: -3 if not);
+ * A is updated in place except the block rows j0..j0+jb-1 (which hpl_factor
+ * overwrites with the DTRSM result).  j0 must be a multiple of NB. */
+int hplk_rs_exchange(int64_t rows, int64_t cols, double *A, int64_t lda, int32_t NB, int32_t P,
+                     int64_t j0, int64_t jb, const int64_t *ipiv, double *U, int64_t ldu);
+
 /* a10 back substitution U x = y, U (N x N upper, row-major ldu), block NB. */
 int hplk_back_solve(int64_t N, int32_t NB, const double *U, int64_t ldu, const double *y,
                     double *x);

@@ -10,5 +10,5 @@ from .hpl import (  # noqa: F401
     hpl_plan_iteration, hpl_plan_fact, hpl_load_local, hpl_regenerate, hpl_residual,
     hpl_set_option, hpl_set_timing, hpl_solve, run_ranks,
     hplk_back_solve, hplk_dgemm_bench, hplk_dgemm_update, hplk_dmma_peak, hplk_panel_bench,
-    hplk_generate, hplk_laswp, hplk_panel_fact, hplk_residual, hplk_trsm,
+    hplk_generate, hplk_laswp, hplk_panel_fact, hplk_residual, hplk_rs_exchange, hplk_trsm,
 )

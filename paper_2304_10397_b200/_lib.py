@@ -69,6 +69,7 @@ _sig("hplk_panel_fact", ctypes.c_int, [i64, i64, vp, i64, vp, i32, i32, i32, i32
                                        ctypes.POINTER(i64)])
 _sig("hplk_laswp", ctypes.c_int, [i64, i64, vp, i64, i64, i64, vp, i64, i64, vp, i64])
 _sig("hplk_back_solve", ctypes.c_int, [i64, i32, vp, i64, vp, vp])
+_sig("hplk_rs_exchange", ctypes.c_int, [i64, i64, vp, i64, i32, i32, i64, i64, vp, vp, i64])
 _sig("hplk_generate", ctypes.c_int, [u64, i64, i64, i64, i64, i64, vp])
 _sig("hplk_residual", ctypes.c_int, [u64, i64, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_double)])
 _sig("hplk_dgemm_bench", ctypes.c_int, [i64, i64, i64, i32, i32, vp])
@@ -81,7 +82,7 @@ EXPORTED = [
     "hpl_last_error", "hpl_singular_column", "hpl_get_ipiv", "hpl_get_local",
     "hpl_get_timeline", "hpl_get_fact_detail", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
     "hpl_last_timing", "hpl_phase_stats", "hpl_debug_state", "hpl_plan_iteration", "hpl_plan_fact", "hpl_pin_host",
-    "hplk_dgemm_update", "hplk_trsm", "hplk_panel_fact", "hplk_laswp", "hplk_back_solve",
+    "hplk_dgemm_update", "hplk_trsm", "hplk_panel_fact", "hplk_laswp", "hplk_rs_exchange", "hplk_back_solve",
     "hplk_generate", "hplk_residual", "hplk_dgemm_bench", "hplk_dmma_peak", "hplk_panel_bench",
 ]
 

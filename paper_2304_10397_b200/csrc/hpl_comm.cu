@@ -131,6 +131,9 @@ hpl_status alloc_ctx(hpl_ctx *c)
         CK(c, cudaMemset(c->cb->flag, 0, sizeof(c->cb->flag)));
     }
     CK(c, fact_work_alloc(&c->fw));
+    CK(c, dgemm_prepare());
+    CK(c, fact_prepare());
+    CK(c, solve_prepare());
     if (c->loop) {
         // every rank's cooperative leaf must fit on the device at once (the
         // P leaves of a column wait on each other): a share of the SMs each

@@ -363,6 +363,14 @@ inline double scaled_residual(const double *h, int64_t N)
     return r == r ? r : __builtin_inf();
 }
 
+// Set every kernel attribute (dynamic shared memory sizes, cluster
+// permissions) once per process, before any rank runs: the first
+// cudaFuncSetAttribute of a kernel must not happen inside one loopback rank
+// while others' kernels already wait on it (hpl_comm.cu alloc_ctx).
+cudaError_t dgemm_prepare();
+cudaError_t fact_prepare();
+cudaError_t solve_prepare();
+
 // FP64 tensor-pipe ceiling: register-resident DMMA chain on every SM.
 cudaError_t dmma_peak(int iters, int blocks_per_sm, int warps, double *ms, double *flop);
 

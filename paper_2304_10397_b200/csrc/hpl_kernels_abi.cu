@@ -2,6 +2,7 @@
 // exactly the kernels hpl_factor uses for one hot-path step (parity tests).
 #include "hpl_internal.cuh"
 #include "../../include/hpl_kernels.h"
+#include <cstring>
 #include <vector>
 
 using namespace hpl;
@@ -132,6 +133,76 @@ int hplk_laswp(int64_t rows, int64_t cols, double *A, int64_t lda, int64_t j0, i
     KT(cudaMemcpy2D(A, lda * 8, dA.p, dla * 8, cols * 8, rows, cudaMemcpyDeviceToHost));
     if (c1 > c0)
         KT(cudaMemcpy2D(U, ldu * 8, dU.p, dlu * 8, (c1 - c0) * 8, jb, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int hplk_rs_exchange(int64_t rows, int64_t cols, double *A, int64_t lda, int32_t NB, int32_t P,
+                     int64_t j0, int64_t jb, const int64_t *ipiv, double *U, int64_t ldu)
+{
+    if (rows < 1 || cols < 1 || lda < cols || NB < 1 || P < 1 || P > MAX_P || jb < 1 ||
+        jb > 1024 || j0 % NB || j0 + jb > rows || ldu < cols)
+        return -1;
+    std::vector<int64_t> rel(jb);
+    for (int64_t k = 0; k < jb; ++k) {
+        if (ipiv[k] < j0 + k || ipiv[k] >= rows) return -1;
+        rel[k] = ipiv[k] - j0;
+    }
+    // process row p's local rows: global rows g with (g / NB) % P == p, in order
+    const int64_t ld = round_up(cols, 16);
+    std::vector<Dev> dA(P), dU(P), dW(P);
+    std::vector<int64_t> mloc(P);
+    RsPeers pr{};
+    pr.P = P;
+    for (int p = 0; p < P; ++p) {
+        int64_t m = 0;
+        for (int64_t g = 0; g < rows; ++g) m += (g / NB) % P == p;
+        mloc[p] = m;
+        KT(dA[p].alloc(sizeof(double) * ld * std::max<int64_t>(m, 1)));
+        KT(dU[p].alloc(sizeof(double) * ld * jb));
+        KT(dW[p].alloc(sizeof(double) * ld * jb));
+        int64_t l = 0;
+        for (int64_t g = 0; g < rows; ++g)
+            if ((g / NB) % P == p)
+                KT(cudaMemcpy(dA[p].as<double>() + (l++) * ld, A + g * lda, cols * 8,
+                              cudaMemcpyHostToDevice));
+        pr.A[p] = dA[p].as<double>();
+    }
+    Dev dRel, dG, dSrc, dDisp, dN;
+    KT(dRel.alloc(sizeof(int64_t) * jb));
+    KT(dG.alloc(sizeof(int64_t) * jb));
+    KT(dSrc.alloc(sizeof(int64_t) * jb));
+    KT(dDisp.alloc(sizeof(int64_t) * 2 * jb));
+    KT(dN.alloc(sizeof(int)));
+    KT(cudaMemcpy(dRel.p, rel.data(), sizeof(int64_t) * jb, cudaMemcpyHostToDevice));
+    KT(pivot_plan(0, jb, j0, dRel.as<int64_t>(), j0, rows, dG.as<int64_t>(), dSrc.as<int64_t>(),
+                  dDisp.as<int64_t>(), dN.as<int>()));
+    // phase 1 on every process row (the peers' A read in place), then phase 2
+    // — the order the two flag barriers of rs_cols enforce
+    for (int p = 0; p < P; ++p) {
+        pr.myrow = p;
+        KT(rs_gather_peer(0, jb, dSrc.as<int64_t>(), dDisp.as<int64_t>(), dN.as<int>(), pr, ld, 0,
+                          cols, dU[p].as<double>(), ld, dW[p].as<double>(), ld, j0, NB));
+    }
+    for (int p = 0; p < P; ++p)
+        KT(rs_scatter(0, dDisp.as<int64_t>(), dN.as<int>(), dW[p].as<double>(), ld, j0,
+                      dA[p].as<double>(), ld, 0, cols, NB, P, p));
+    KT(cudaDeviceSynchronize());
+    for (int p = 0; p < P; ++p) {
+        int64_t l = 0;
+        for (int64_t g = 0; g < rows; ++g)
+            if ((g / NB) % P == p)
+                KT(cudaMemcpy(A + g * lda, dA[p].as<double>() + (l++) * ld, cols * 8,
+                              cudaMemcpyDeviceToHost));
+    }
+    // every process row gathered the same U: return process row 0's, check the rest
+    KT(cudaMemcpy2D(U, ldu * 8, dU[0].p, ld * 8, cols * 8, jb, cudaMemcpyDeviceToHost));
+    std::vector<double> other((size_t)cols * jb);
+    for (int p = 1; p < P; ++p) {
+        KT(cudaMemcpy2D(other.data(), cols * 8, dU[p].p, ld * 8, cols * 8, jb,
+                        cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < jb; ++k)
+            if (std::memcmp(other.data() + k * cols, U + k * ldu, cols * 8)) return -3;
+    }
     return 0;
 }
 

@@ -828,6 +828,21 @@ void ensure_sms(FactWork *wk)
     }
 }
 
+cudaError_t cluster_attr()
+{
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(leaf_fact_cluster_kernel,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(leaf_fact_cluster_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(sizeof(double) * CL_ROWS * LEAF_MAX));
+    });
+    return attr_err;
+}
+
 // grid of the next leaf launch: {CTAs, threads per CTA} from the context's policy
 void leaf_grid(const FactWork *wk, int64_t rows, int *G, int *NT)
 {
@@ -852,17 +867,7 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t m, double *P, int64_t ldp, int 
         m - k0 <= (int64_t)CL_SIZE * CL_ROWS && w <= LEAF_MAX && w > 0 && m - k0 > 0) {
         const int chunk = (int)cdiv(m - k0, CL_SIZE);
         const size_t smem = sizeof(double) * (size_t)chunk * w;
-        static std::once_flag once;
-        static cudaError_t attr_err = cudaSuccess;
-        std::call_once(once, [] {
-            attr_err = cudaFuncSetAttribute(leaf_fact_cluster_kernel,
-                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (attr_err == cudaSuccess)
-                attr_err = cudaFuncSetAttribute(leaf_fact_cluster_kernel,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(sizeof(double) * CL_ROWS * LEAF_MAX));
-        });
-        cudaError_t e = attr_err;
+        cudaError_t e = cluster_attr();
         if (e == cudaSuccess) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(CL_SIZE);
@@ -968,6 +973,13 @@ cudaError_t rec_fact(cudaStream_t st, int64_t m, int64_t nb, double *P, int64_t 
 }
 
 }  // namespace
+
+cudaError_t fact_prepare()
+{
+    const cudaError_t e = cluster_attr();
+    if (e != cudaSuccess) cudaGetLastError();   // the grid leaf then serves every panel
+    return cudaSuccess;
+}
 
 void fact_set_leaf_ctas(FactWork *w, int max_ctas, int rows_per_cta)
 {

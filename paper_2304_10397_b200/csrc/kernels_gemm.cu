@@ -392,8 +392,7 @@ using CfgB = Cfg<128, 128, 64, 32, 6, 1>;
 using CfgC = Cfg<64, 64, 32, 32, 4, 3>;
 
 template <class C, int SLOT>
-cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
-                        const GemmParams &p)
+cudaError_t set_attr()
 {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -401,7 +400,23 @@ cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMa
         attr_err = cudaFuncSetAttribute(dgemm_tma_kernel<C, SLOT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     });
-    HPL_CUDA_TRY(attr_err);
+    return attr_err;
+}
+
+template <class C>
+cudaError_t set_attr_all()
+{
+    HPL_CUDA_TRY((set_attr<C, SLOT_TRAIL>()));
+    HPL_CUDA_TRY((set_attr<C, SLOT_LOOKAHEAD>()));
+    HPL_CUDA_TRY((set_attr<C, SLOT_FACT>()));
+    return set_attr<C, SLOT_RS>();
+}
+
+template <class C, int SLOT>
+cudaError_t launch_slot(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
+                        const GemmParams &p)
+{
+    HPL_CUDA_TRY((set_attr<C, SLOT>()));
     ParamPad<SLOT> pad{};
     const unsigned grid = (unsigned)(p.pair_lower ? p.ntiles / 2 : p.ntiles);
     dgemm_tma_kernel<C, SLOT><<<grid, C::THREADS, C::SMEM, st>>>(p, pad, ma, mb);
@@ -426,6 +441,14 @@ cudaError_t launch_cfg(cudaStream_t st, const CUtensorMap &ma, const CUtensorMap
 }
 
 }  // namespace
+
+cudaError_t dgemm_prepare()
+{
+    if (!get_encode()) return cudaErrorNotSupported;
+    HPL_CUDA_TRY(set_attr_all<CfgA>());
+    HPL_CUDA_TRY(set_attr_all<CfgB>());
+    return set_attr_all<CfgC>();
+}
 
 cudaError_t dgemm(cudaStream_t st, int mode, bool a_lower, int64_t m, int64_t n, int64_t k,
                   const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

@@ -471,6 +471,28 @@ std::atomic<bool> g_bs_cluster_ok{true};   // cleared once if the device cannot 
 
 bool bs_diag_folds_near(int nb) { return g_bs_cluster_ok && nb <= BSC_CTAS * BSC_ROWS; }
 
+cudaError_t bs_cluster_attr()
+{
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+        attr = cudaFuncSetAttribute(bs_diag_cluster_kernel,
+                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (attr == cudaSuccess)
+            attr = cudaFuncSetAttribute(bs_diag_cluster_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(double) * BSC_ROWS * BSC_LD));
+    });
+    if (attr != cudaSuccess) g_bs_cluster_ok = false;
+    return attr;
+}
+
+cudaError_t solve_prepare()
+{
+    if (bs_cluster_attr() != cudaSuccess) cudaGetLastError();
+    return cudaSuccess;
+}
+
 int bs_splits(int nb, int64_t lc_lo, int64_t lc_hi, int NB)
 {
     if (lc_hi <= lc_lo || nb <= 0) return 1;
@@ -507,17 +529,8 @@ cudaError_t bs_diag(cudaStream_t st, int nb, const double *Ubb, int64_t ldu,
     if (nb <= 0) return cudaSuccess;
     if (nb > BS_MAXB) return cudaErrorInvalidValue;
     if (nb <= BSC_CTAS * BSC_ROWS && g_bs_cluster_ok) {
-        static std::once_flag once;
-        static cudaError_t attr = cudaSuccess;
         const int smem = (int)(sizeof(double) * BSC_ROWS * BSC_LD);
-        std::call_once(once, [smem] {
-            attr = cudaFuncSetAttribute(bs_diag_cluster_kernel,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (attr == cudaSuccess)
-                attr = cudaFuncSetAttribute(bs_diag_cluster_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        });
-        cudaError_t e = attr;
+        cudaError_t e = bs_cluster_attr();
         if (e == cudaSuccess) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(BSC_CTAS);

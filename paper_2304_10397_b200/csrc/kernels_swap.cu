@@ -174,23 +174,47 @@ rs_pack_kernel(int jb, const int64_t *__restrict__ src, const double *__restrict
 }
 
 // A[local(d)][c0 + c] = W[s - j0][c] for the displaced pairs (d, s) this process row owns;
-// W holds the original block row j (broadcast from its owner).
+// W holds the original block row j (from its owner).  The owned pairs are
+// compacted in shared memory first, then LS_UNROLL rows per warp are in flight.
 __global__ void __launch_bounds__(LS_WARPS * 32)
 rs_scatter_kernel(const int64_t *__restrict__ disp, const int *__restrict__ ndisp,
                   const double *__restrict__ W, long long ldw, long long j0, double *A,
-                  long long lda, long long c0, long long c1, int NB, int P, int myrow)
+                  long long lda, long long c0, long long c1, int NB, int P, int myrow, int vec)
 {
+    __shared__ long long s_dst[LS_MAXJB], s_w[LS_MAXJB];   // s_dst < 0: not this process row's
+    const int nd = *ndisp;
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+        const long long g = disp[2 * d];
+        const bool mine = owns_row(g, NB, P, myrow);
+        s_dst[d] = mine ? g2l_row(g, NB, P) : -1;
+        s_w[d] = disp[2 * d + 1] - j0;
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long col = c0 + (long long)blockIdx.x * LS_COLS + 2 * lane;
     const bool has0 = col < c1, has1 = col + 1 < c1;
-    const int nd = *ndisp;
-    for (int d = warp; d < nd; d += LS_WARPS) {
-        const long long g = disp[2 * d];
-        if (!owns_row(g, NB, P, myrow)) continue;
-        const double *sp = W + (disp[2 * d + 1] - j0) * ldw + (col - c0);
-        double *t = A + g2l_row(g, NB, P) * lda + col;
-        if (has0) t[0] = sp[0];
-        if (has1) t[1] = sp[1];
+    const int total = nd;
+    for (int k0 = warp * LS_UNROLL; k0 < total; k0 += LS_WARPS * LS_UNROLL) {
+        if (vec && has1) {
+            double2 v[LS_UNROLL];
+#pragma unroll
+            for (int u = 0; u < LS_UNROLL; ++u)
+                if (k0 + u < total && s_dst[k0 + u] >= 0)
+                    v[u] = *reinterpret_cast<const double2 *>(W + s_w[k0 + u] * ldw + (col - c0));
+#pragma unroll
+            for (int u = 0; u < LS_UNROLL; ++u)
+                if (k0 + u < total && s_dst[k0 + u] >= 0)
+                    *reinterpret_cast<double2 *>(A + s_dst[k0 + u] * lda + col) = v[u];
+        } else {
+#pragma unroll
+            for (int u = 0; u < LS_UNROLL; ++u)
+                if (k0 + u < total && s_dst[k0 + u] >= 0) {
+                    const double *sp = W + s_w[k0 + u] * ldw + (col - c0);
+                    double *t = A + s_dst[k0 + u] * lda + col;
+                    if (has0) t[0] = sp[0];
+                    if (has1) t[1] = sp[1];
+                }
+        }
     }
 }
 
@@ -228,63 +252,58 @@ __global__ void flag_kernel(FlagOp op, SpinCtl sc)
     __threadfence_system();
 }
 
-constexpr int RG_UNROLL = 4;
-
+// Phase 1 of the peer-memory RS: the plan (which row of which peer lands in
+// which row of U or W) is resolved once per CTA into shared memory, then each
+// warp keeps LS_UNROLL 16-byte row copies in flight (peer rows come over
+// NVLink; the reads bypass L1: __ldcg).
 __global__ void __launch_bounds__(LS_WARPS * 32)
 rs_gather_peer_kernel(int jb, const int64_t *__restrict__ src, const int64_t *__restrict__ disp,
                       const int *__restrict__ ndisp, RsPeers pr, long long lda, long long c0,
                       long long c1, double *__restrict__ U, long long ldu,
                       double *__restrict__ W, long long ldw, long long j0, int NB, int vec)
 {
+    // entries [0, jb): U rows; [jb, jb + nd): displaced pairs (null when the
+    // displaced row is not this process row's)
+    __shared__ const double *s_src[2 * LS_MAXJB];
+    __shared__ double *s_dst[2 * LS_MAXJB];
+    const int P = pr.P;
+    const int bowner = (int)((j0 / NB) % P);
+    const int nd = *ndisp;
+    for (int k = threadIdx.x; k < jb; k += blockDim.x) {
+        const long long g = src[k];
+        s_src[k] = pr.A[(int)((g / NB) % P)] + g2l_row(g, NB, P) * lda;
+        s_dst[k] = U + (long long)k * ldu - c0;
+    }
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+        const long long dg = disp[2 * d], sg = disp[2 * d + 1];
+        const bool mine = owns_row(dg, NB, P, pr.myrow);
+        s_src[jb + d] = mine ? pr.A[bowner] + g2l_row(sg, NB, P) * lda : nullptr;
+        s_dst[jb + d] = W + (sg - j0) * ldw - c0;
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long col = c0 + (long long)blockIdx.x * LS_COLS + 2 * lane;
     const bool has0 = col < c1, has1 = col + 1 < c1;
-    const int P = pr.P;
-    // row k of U (k < jb) or, for k >= jb, the displaced row slot k - jb
-    const int nd = *ndisp;
-    const int bowner = (int)((j0 / NB) % P);
     const int total = jb + nd;
-    for (int k0 = warp * RG_UNROLL; k0 < total; k0 += LS_WARPS * RG_UNROLL) {
-        const double *sp[RG_UNROLL];
-        double *dp[RG_UNROLL];
-#pragma unroll
-        for (int u = 0; u < RG_UNROLL; ++u) {
-            const int k = k0 + u;
-            sp[u] = nullptr;
-            dp[u] = nullptr;
-            if (k < jb) {
-                const long long g = src[k];
-                sp[u] = pr.A[(int)((g / NB) % P)] + g2l_row(g, NB, P) * lda + col;
-                dp[u] = U + (long long)k * ldu + (col - c0);
-            } else if (k < total) {
-                const long long d = disp[2 * (k - jb)], s = disp[2 * (k - jb) + 1];
-                if (owns_row(d, NB, P, pr.myrow)) {
-                    sp[u] = pr.A[bowner] + g2l_row(s, NB, P) * lda + col;
-                    dp[u] = W + (s - j0) * ldw + (col - c0);
-                }
-            }
-        }
+    for (int k0 = warp * LS_UNROLL; k0 < total; k0 += LS_WARPS * LS_UNROLL) {
         if (vec && has1) {
-            double2 v[RG_UNROLL];
+            double2 v[LS_UNROLL];
 #pragma unroll
-            for (int u = 0; u < RG_UNROLL; ++u)
-                if (sp[u]) v[u] = __ldcg(reinterpret_cast<const double2 *>(sp[u]));
+            for (int u = 0; u < LS_UNROLL; ++u)
+                if (k0 + u < total && s_src[k0 + u])
+                    v[u] = __ldcg(reinterpret_cast<const double2 *>(s_src[k0 + u] + col));
 #pragma unroll
-            for (int u = 0; u < RG_UNROLL; ++u)
-                if (sp[u]) *reinterpret_cast<double2 *>(dp[u]) = v[u];
+            for (int u = 0; u < LS_UNROLL; ++u)
+                if (k0 + u < total && s_src[k0 + u])
+                    *reinterpret_cast<double2 *>(s_dst[k0 + u] + col) = v[u];
         } else {
-            double v0[RG_UNROLL], v1[RG_UNROLL];
 #pragma unroll
-            for (int u = 0; u < RG_UNROLL; ++u)
-                if (sp[u]) {
-                    v0[u] = has0 ? __ldcg(sp[u]) : 0.0;
-                    v1[u] = has1 ? __ldcg(sp[u] + 1) : 0.0;
-                }
-#pragma unroll
-            for (int u = 0; u < RG_UNROLL; ++u)
-                if (sp[u]) {
-                    if (has0) dp[u][0] = v0[u];
-                    if (has1) dp[u][1] = v1[u];
+            for (int u = 0; u < LS_UNROLL; ++u)
+                if (k0 + u < total && s_src[k0 + u]) {
+                    const double *sp = s_src[k0 + u] + col;
+                    double *dp = s_dst[k0 + u] + col;
+                    if (has0) dp[0] = __ldcg(sp);
+                    if (has1) dp[1] = __ldcg(sp + 1);
                 }
         }
     }
@@ -307,8 +326,10 @@ cudaError_t rs_scatter(cudaStream_t st, const int64_t *disp, const int *ndisp, c
                        int NB, int P, int myrow)
 {
     if (c1 <= c0) return cudaSuccess;
+    const int vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15) == 0 &&
+                    (lda & 1) == 0 && (ldw & 1) == 0 && (c0 & 1) == 0;
     rs_scatter_kernel<<<(unsigned)cdiv(c1 - c0, LS_COLS), LS_WARPS * 32, 0, st>>>(
-        disp, ndisp, W, ldw, j0, A, lda, c0, c1, NB, P, myrow);
+        disp, ndisp, W, ldw, j0, A, lda, c0, c1, NB, P, myrow, vec);
     count_launch();
     return cudaGetLastError();
 }
@@ -328,6 +349,7 @@ cudaError_t rs_gather_peer(cudaStream_t st, int64_t jb, const int64_t *src, cons
                            int NB)
 {
     if (jb <= 0 || c1 <= c0) return cudaSuccess;
+    if (jb > LS_MAXJB) return cudaErrorInvalidValue;
     bool vec = (lda & 1) == 0 && (c0 & 1) == 0 && (ldu & 1) == 0 && (ldw & 1) == 0 &&
                (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&
                (reinterpret_cast<uintptr_t>(W) & 15) == 0;

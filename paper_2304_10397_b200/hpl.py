@@ -314,6 +314,19 @@ def hplk_laswp(A, j0: int, ipiv, c0: int = 0, c1: int | None = None):
     return A, U[:, : c1 - c0]
 
 
+def hplk_rs_exchange(A, NB: int, P: int, j0: int, ipiv):
+    """Device RS over P emulated process rows (rs_gather_peer + rs_scatter).
+    Returns (A_after, U) like hplk_laswp (block rows of A left as they were)."""
+    A = np.ascontiguousarray(A, dtype=np.float64).copy()
+    rows, cols = A.shape
+    ipiv = np.ascontiguousarray(ipiv, dtype=np.int64)
+    jb = len(ipiv)
+    U = np.zeros((jb, cols), dtype=np.float64)
+    _k(lib.hplk_rs_exchange(rows, cols, ptr(A), cols, NB, P, j0, jb, ptr(ipiv), ptr(U), cols),
+       "hplk_rs_exchange")
+    return A, U
+
+
 def hplk_back_solve(U, y, NB: int = 64):
     U = np.ascontiguousarray(U, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)

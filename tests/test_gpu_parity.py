@@ -206,6 +206,28 @@ def test_laswp_bitwise(H, rows, cols, j0, jb, c0, c1):
     assert np.array_equal(A_gpu[:, :c0], A[:, :c0]) and np.array_equal(A_gpu[:, c1:], A[:, c1:])
 
 
+@pytest.mark.parametrize("rows,cols,NB,P,j0,jb", [(1000, 300, 64, 2, 128, 64), (2000, 517, 32, 4, 64, 32),
+                                                  (777, 129, 16, 3, 0, 16), (4096, 1000, 256, 2, 1024, 256),
+                                                  (3000, 64, 128, 8, 512, 128)])
+def test_rs_exchange_bitwise(H, rows, cols, NB, P, j0, jb):
+    """a2/a3: the P > 1 row swaps (rs_gather_peer reading the owners'
+    buffers, then rs_scatter) over P emulated process rows give exactly the
+    oracle's sequential swaps — bit for bit, pivots that
+    cross process rows included."""
+    rng = np.random.default_rng(rows + P)
+    A = rng.standard_normal((rows, cols))
+    ipiv = random_ipiv(rows, j0, jb, seed=cols + P)
+    A_gpu, Ug = H.hplk_rs_exchange(A, NB, P, j0, ipiv)
+    full_ipiv = np.arange(rows, dtype=np.int64)
+    full_ipiv[j0:j0 + jb] = ipiv
+    ref = oracle.laswp(A, j0, j0 + jb, full_ipiv)
+    assert np.array_equal(Ug, ref[j0:j0 + jb])
+    outside = np.ones(rows, bool)
+    outside[j0:j0 + jb] = False
+    assert np.array_equal(A_gpu[outside], ref[outside])
+    assert np.array_equal(A_gpu[j0:j0 + jb], A[j0:j0 + jb])
+
+
 def test_laswp_identity_moves_nothing(H):
     A = np.random.default_rng(2).standard_normal((64, 40))
     A_gpu, Ug = H.hplk_laswp(A, 8, np.arange(8, 24), 0, 40)
