@@ -133,6 +133,18 @@ hpl_status hpl_regenerate(hpl_ctx *ctx);
  * timing and tests with hand-made systems.  Returns to "initialised". */
 hpl_status hpl_load_local(hpl_ctx *ctx, const double *host, int64_t ld);
 
+/* hpl_load_local + hpl_factor with the host->device copy overlapped with
+ * the factorization (one-rank contexts; several ranks fall back to the two
+ * calls).  The local block is copied in column chunks on a copy stream and
+ * the updates of the first iterations run per chunk behind the arrivals
+ * (DESIGN.md §5 "Pipelined start"), so most of the copy hides behind the
+ * DGEMMs; the arithmetic per element is unchanged, the result is bitwise that
+ * of the two calls.  `host` should be page-locked (hpl_pin_host) for the copy
+ * to be asynchronous; it is read during the call only.  Collective; returns
+ * like hpl_factor; afterwards the context holds a loaded system
+ * (hpl_residual: HPL_ERR_STATE). */
+hpl_status hpl_load_factor(hpl_ctx *ctx, const double *host, int64_t ld);
+
 /* Local extents of [A | b] on this rank (rows, cols incl. b when owned). */
 hpl_status hpl_local_shape(const hpl_ctx *ctx, int64_t *rows, int64_t *cols);
 
@@ -198,13 +210,16 @@ hpl_status hpl_last_timing(const hpl_ctx *ctx, double *out6);
 
 /* Per-phase totals of the last hpl_factor / hpl_solve (CUDA events; the
  * factor entries need hpl_set_timing(1)), for the roofline of every
- * non-DGEMM kernel: out8 = {rest LASWP/RS ms, its algorithmic bytes
+ * non-DGEMM kernel: out10 = {rest LASWP/RS ms, its algorithmic bytes
  * (2 x 8 x (jb + displaced rows) x rest columns per iteration: each moved
  * row read once and written once), rest DTRSM ms, its flop (jb^2 x rest
  * columns per iteration), FACT ms (owner column, summed over panels), solve
  * ms, the solve's algorithmic bytes (this rank's part of the upper triangle
- * of U, read once), trailing-DGEMM ms}. */
-hpl_status hpl_phase_stats(const hpl_ctx *ctx, double *out8);
+ * of U, read once), trailing-DGEMM ms, and for hpl_load_factor: ms from the
+ * factorization's start until the last column chunk landed, bytes copied,
+ * ms until the pipelined start's iterations were done everywhere, their
+ * number (0, 0, 0, 0 otherwise)} — 12 doubles. */
+hpl_status hpl_phase_stats(const hpl_ctx *ctx, double *out10);
 
 /* Debug hook: out = {group barrier counters (world, row, column, column-tr),
  * this rank's 4 x 32 group flag words (arrivals received per group and

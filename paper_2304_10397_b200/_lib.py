@@ -44,6 +44,7 @@ _sig("hpl_solve", ctypes.c_int, [ctx_p, vp])
 _sig("hpl_residual", ctypes.c_int, [ctx_p, ctypes.POINTER(ctypes.c_double)])
 _sig("hpl_regenerate", ctypes.c_int, [ctx_p])
 _sig("hpl_load_local", ctypes.c_int, [ctx_p, vp, i64])
+_sig("hpl_load_factor", ctypes.c_int, [ctx_p, vp, i64])
 _sig("hpl_local_shape", ctypes.c_int, [ctx_p, ctypes.POINTER(i64), ctypes.POINTER(i64)])
 _sig("hpl_free", None, [ctx_p])
 _sig("hpl_last_error", ctypes.c_char_p, [ctx_p])
@@ -78,7 +79,7 @@ _sig("hplk_panel_bench", ctypes.c_int, [i64, i64, i32, i32, i32, vp])
 
 EXPORTED = [
     "hpl_init", "hpl_init_dist", "hpl_init_loopback", "hpl_get_unique_id", "hpl_factor", "hpl_solve",
-    "hpl_residual", "hpl_regenerate", "hpl_load_local", "hpl_local_shape", "hpl_free",
+    "hpl_residual", "hpl_regenerate", "hpl_load_local", "hpl_load_factor", "hpl_local_shape", "hpl_free",
     "hpl_last_error", "hpl_singular_column", "hpl_get_ipiv", "hpl_get_local",
     "hpl_get_timeline", "hpl_get_fact_detail", "hpl_set_timing", "hpl_set_option", "hpl_launch_count",
     "hpl_last_timing", "hpl_phase_stats", "hpl_debug_state", "hpl_plan_iteration", "hpl_plan_fact", "hpl_pin_host",

@@ -76,7 +76,17 @@ hpl_status alloc_ctx(hpl_ctx *c)
     };
     const size_t NBs = (size_t)c->NB;
     if (!M((void **)&c->A, sizeof(double) * (size_t)c->mloc * c->lda)) return HPL_ERR_OOM;
-    for (int b = 0; b < hpl_ctx::NBUF; ++b) {
+    c->nbuf = hpl_ctx::NBUF;
+    if (c->nranks == 1) {
+        // one rank: MAXBUF panel states if they leave >= 4 GB free
+        size_t fr = 0, tot = 0;
+        const size_t per = sizeof(double) * ((size_t)c->ldp * (NBs + 1) + (size_t)c->ldlinv * NBs);
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
+            fr > per * hpl_ctx::MAXBUF + 2 * sizeof(double) * NBs * c->ldu + ((size_t)4 << 30))
+            c->nbuf = hpl_ctx::MAXBUF;
+        cudaGetLastError();
+    }
+    for (int b = 0; b < c->nbuf; ++b) {
         if (!M((void **)&c->panel[b], sizeof(double) * (size_t)c->ldp * (NBs + 1))) return HPL_ERR_OOM;
         if (!M((void **)&c->linv[b], sizeof(double) * (size_t)c->ldlinv * NBs)) return HPL_ERR_OOM;
         if (!M((void **)&c->src[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
@@ -151,7 +161,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     for (cudaEvent_t *e : {&c->ev_rsR, &c->ev_rsL, &c->ev_dgR, &c->ev_dgL, &c->ev_next,
                            &c->ev_rest, &c->ev_trsm})
         CK(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    for (int b = 0; b < hpl_ctx::NBUF; ++b)
+    for (int b = 0; b < c->nbuf; ++b)
         CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
     for (int k = 0; k < 3; ++k) CK(c, cudaEventCreate(&c->ev_t[k]));
     return HPL_OK;
@@ -314,7 +324,7 @@ void release(hpl_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaFree(c->A);
-    for (int b = 0; b < hpl_ctx::NBUF; ++b) {
+    for (int b = 0; b < hpl_ctx::MAXBUF; ++b) {
         cudaFree(c->panel[b]); cudaFree(c->linv[b]);
         cudaFree(c->src[b]); cudaFree(c->disp[b]); cudaFree(c->ndisp[b]);
         if (c->ev_panel[b]) cudaEventDestroy(c->ev_panel[b]);
@@ -341,8 +351,9 @@ void release(hpl_ctx *c)
     for (auto e : c->tev) cudaEventDestroy(e);
     for (int k = 0; k < 3; ++k)
         if (c->ev_t[k]) cudaEventDestroy(c->ev_t[k]);
-    for (cudaStream_t s : {c->s_la, c->s_tr, c->s_rs})
+    for (cudaStream_t s : {c->s_la, c->s_tr, c->s_rs, c->s_h2d})
         if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : c->ev_arr) cudaEventDestroy(e);
 }
 
 namespace {

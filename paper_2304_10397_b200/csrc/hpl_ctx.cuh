@@ -81,14 +81,20 @@ struct hpl_ctx {
     // local storage
     int64_t mloc = 0, nloc = 0, lda = 0;
     double *A = nullptr;
-    static constexpr int NBUF = 3;   // per-panel state: panels j, j+1, j+2 live at once
-    double *panel[NBUF] = {};
+    // per-panel state (panel, L11^{-1}, pivot plan): panels j, j+1, j+2 are
+    // live at once in the look-ahead loop.  NBUF = 3 buffers where peers index
+    // them (P*Q > 1: the LBCAST pull and the gathered FACT read buffer j mod 3);
+    // a one-rank context keeps MAXBUF (memory permitting) so hpl_load_factor's
+    // pipelined start can have K + 1 panels in flight (nbuf = buffers in use).
+    static constexpr int NBUF = 3, MAXBUF = 8;
+    int nbuf = NBUF;
+    double *panel[MAXBUF] = {};
     int64_t ldp = 0;
-    double *linv[NBUF] = {};
+    double *linv[MAXBUF] = {};
     int64_t ldlinv = 0;
-    int64_t *src[NBUF] = {};
-    int64_t *disp[NBUF] = {};
-    int *ndisp[NBUF] = {};
+    int64_t *src[MAXBUF] = {};
+    int64_t *disp[MAXBUF] = {};
+    int *ndisp[MAXBUF] = {};
     int64_t *gpiv = nullptr;
     double *U = nullptr;     // gathered block rows (pre-DTRSM), NB x ldu
     double *U2 = nullptr;    // L11^{-1} U (the DGEMM's B operand), NB x ldu
@@ -103,7 +109,11 @@ struct hpl_ctx {
     double *hstage = nullptr;
     hpl::FactWork fw{};
     cudaStream_t s_la = nullptr, s_tr = nullptr, s_rs = nullptr;
-    cudaEvent_t ev_panel[NBUF] = {}, ev_rest = nullptr;
+    cudaEvent_t ev_panel[MAXBUF] = {}, ev_rest = nullptr;
+    // hpl_load_factor's pipelined start: copy stream and one arrival event
+    // per column chunk (created on first use)
+    cudaStream_t s_h2d = nullptr;
+    std::vector<cudaEvent_t> ev_arr;
     cudaEvent_t ev_next = nullptr;   // rest(j) has updated panel j+2's columns
     cudaEvent_t ev_trsm = nullptr;   // rest(j)'s LASWP+DTRSM done: FACT(j+1) may start
     cudaEvent_t ev_rsR = nullptr, ev_rsL = nullptr, ev_dgR = nullptr, ev_dgL = nullptr;
@@ -127,6 +137,10 @@ struct hpl_ctx {
     double laswp_ms = 0, laswp_bytes = 0;  // rest RS/LASWP phases, timing on
     double trsm_ms = 0, trsm_flop = 0;     // rest DTRSM phases, timing on
     double fact_ms = 0;                    // FACT(j+1) proper, summed, timing on
+    double h2d_ms = 0, h2d_bytes = 0;      // hpl_load_factor: factor start -> last chunk landed
+    int h2d_last = -1;
+    double pstart_ms = 0;                  // factor start -> end of the pipelined start
+    int pstart_k = 0;                      // iterations in the pipelined start
     // state
     enum { S_NONE, S_INIT, S_FACTORED, S_SOLVED, S_BROKEN } state = S_NONE;
     bool loaded = false;             // [A | b] came from hpl_load_local (not the seeded system)

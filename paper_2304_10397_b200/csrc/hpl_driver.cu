@@ -377,18 +377,97 @@ bool usable(hpl_ctx *c, int want, const char *who)
     return c->state == want;
 }
 
-}  // namespace
+// The local [A | b] arriving from a host buffer (hpl_load_factor).
+struct Arrival {
+    const double *host;
+    int64_t ld;
+};
 
-extern "C" {
-
-hpl_status hpl_factor(hpl_ctx *c)
+// Pipelined start (hpl_load_factor, one rank): the local matrix is copied in
+// column chunks (whole NB blocks) on a copy stream while the first K
+// iterations run chunk by chunk, in chunk-major order on S_la: chunk 0 —
+// which holds panels 0..K — is factored and updated first (FACT(j+1) right
+// after update(j) of chunk 0, each with the whole GPU), then every later chunk
+// receives its K updates as soon as it has landed.  Per column the same
+// kernels run in the same order as in the look-ahead loop, so the result is
+// bitwise that of hpl_load_local + hpl_factor (tested); the copy of the
+// later chunks hides behind the earlier chunks' updates.  (A first version
+// ran every chunk on its own stream: the FACT chain's kernels, which need
+// whole SMs, starved behind the stream of DGEMM CTAs — FACT(1) ready at
+// 0.23 s finished at 1.59 s — DESIGN.md §5.)  On return FACT(K) is done.
+hpl_status pipelined_start(hpl_ctx *c, const Arrival &a, int64_t *jstart)
 {
-    if (!c) return HPL_ERR_ARG;
-    if (!usable(c, hpl_ctx::S_INIT, "hpl_factor")) {
-        if (c->state != hpl_ctx::S_BROKEN)
-            set_err(c, "hpl_factor: context not in the initialised state");
-        return HPL_ERR_STATE;
+    const int64_t nblk = cdiv(c->N, c->NB);
+    const int K = (int)std::min<int64_t>(std::min<int64_t>(6, c->nbuf - 1), nblk - 1);
+    const int64_t nbl_cols = cdiv(c->nloc, c->NB);            // local column blocks (b included)
+    // chunk 0 holds panels 0..K; about 16 chunks in all
+    const int64_t per = std::max<int64_t>(K + 1, cdiv(nbl_cols, 16)) * c->NB;
+    std::vector<int64_t> cb;
+    for (int64_t x = 0; x < c->nloc; x += per) cb.push_back(x);
+    cb.push_back(c->nloc);
+    const int nc = (int)cb.size() - 1;
+    int lo_p, hi_p;
+    CK(c, cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+    if (!c->s_h2d) CK(c, cudaStreamCreateWithPriority(&c->s_h2d, cudaStreamNonBlocking, lo_p));
+    while ((int)c->ev_arr.size() < nc) {
+        cudaEvent_t e;
+        CK(c, cudaEventCreate(&e));                  // timed: hpl_phase_stats h2d_ms
+        c->ev_arr.push_back(e);
     }
+    CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_t[0], 0));
+    for (int k = 0; k < nc; ++k) {
+        CK(c, cudaMemcpy2DAsync(c->A + cb[k], c->lda * 8, a.host + cb[k], a.ld * 8,
+                                (cb[k + 1] - cb[k]) * 8, c->mloc, cudaMemcpyHostToDevice,
+                                c->s_h2d));
+        CK(c, cudaEventRecord(c->ev_arr[k], c->s_h2d));
+    }
+    cudaStream_t st = c->s_la;
+    const bool auto0 = c->leaf_auto;
+    const int lmax0 = c->fw.leaf_max_ctas, lrows0 = c->fw.leaf_rows_per_cta, lwarp0 = c->fw.leaf_warp_ctas;
+    auto update = [&](int64_t j, int k) -> hpl_status {
+        const int b = (int)(j % c->nbuf);
+        const int64_t lo = std::max(lcols_before(c, j * c->NB + jb_of(c, j)), cb[k]);
+        const int64_t hi = cb[k + 1];
+        if (lo >= hi) return HPL_OK;
+        RsOut rs;
+        ST(rs_cols(c, st, j, b, lo, hi, SEC_RIGHT, &rs));
+        return compute_cols(c, st, j, b, lo, hi, rs, true, true, c->timing);
+    };
+    // chunk 0: FACT(0), then update(j) and FACT(j+1) for j < K — alone on the
+    // GPU, so the leaf gets every SM
+    c->leaf_auto = false;
+    fact_set_leaf_ctas(&c->fw, 0, 512);
+    c->fw.leaf_warp_ctas = 0;
+    CK(c, cudaStreamWaitEvent(st, c->ev_arr[0], 0));
+    ST(fact_panel(c, st, 0, 0));
+    for (int64_t j = 0; j < K; ++j) {
+        ST(update(j, 0));
+        ST(fact_panel(c, st, j + 1, (int)((j + 1) % c->nbuf)));
+    }
+    c->leaf_auto = auto0;
+    c->fw.leaf_max_ctas = lmax0;
+    c->fw.leaf_rows_per_cta = lrows0;
+    c->fw.leaf_warp_ctas = lwarp0;
+    CK(c, cudaEventRecord(c->ev_panel[K % c->nbuf], st));
+    for (int k = 1; k < nc; ++k) {
+        CK(c, cudaStreamWaitEvent(st, c->ev_arr[k], 0));
+        for (int64_t j = 0; j < K; ++j) ST(update(j, k));
+    }
+    c->h2d_bytes = 8.0 * (double)c->mloc * (double)c->nloc;
+    c->h2d_last = nc - 1;
+    // the look-ahead loop continues from iteration K on the whole matrix
+    CK(c, cudaEventRecord(c->ev_rest, st));
+    CK(c, cudaStreamWaitEvent(c->s_tr, c->ev_rest, 0));
+    CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_rest, 0));
+    CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
+    CK(c, cudaEventRecord(c->ev_t[2], st));          // end of the pipelined start (stats)
+    c->pstart_k = K;
+    *jstart = K;
+    return HPL_OK;
+}
+
+hpl_status factor_impl(hpl_ctx *c, const Arrival *arr)
+{
     CK(c, cudaSetDevice(c->device));
     trace(c, "factor start");
     const int64_t l0 = t_launches;
@@ -403,8 +482,14 @@ hpl_status hpl_factor(hpl_ctx *c)
     CK(c, cudaStreamWaitEvent(c->s_rs, c->ev_t[0], 0));
     CK(c, cudaEventRecord(c->ev_rest, c->s_tr));
     CK(c, fill_u64(c->s_la, reinterpret_cast<unsigned long long *>(c->fw.info), ~0ull));
-    ST(fact_panel(c, c->s_la, 0, 0));
-    CK(c, cudaEventRecord(c->ev_panel[0], c->s_la));
+    int64_t jstart = 0;
+    c->h2d_last = -1;
+    if (arr) {
+        ST(pipelined_start(c, *arr, &jstart));
+    } else {
+        ST(fact_panel(c, c->s_la, 0, 0));
+        CK(c, cudaEventRecord(c->ev_panel[0], c->s_la));
+    }
     // split update (option "split" = right-section percent; the paper uses 50 %,
     // PAPER.md l.66).  Default off: measured neutral on B200.
     const bool split = c->lookahead && c->split_pct > 0;
@@ -418,8 +503,8 @@ hpl_status hpl_factor(hpl_ctx *c)
     }
     int *nd_hist = nullptr;       // displaced rows per panel (LASWP bytes), timing only
     if (c->timing) CK(c, cudaMallocAsync((void **)&nd_hist, sizeof(int) * nblk, c->s_la));
-    for (int64_t j = 0; j < nblk; ++j) {
-        const int b = (int)(j % hpl_ctx::NBUF), bn = (int)((j + 1) % hpl_ctx::NBUF);
+    for (int64_t j = jstart; j < nblk; ++j) {
+        const int b = (int)(j % c->nbuf), bn = (int)((j + 1) % c->nbuf);
         const int64_t j0 = j * c->NB, jb = jb_of(c, j);
         const int64_t lct = lcols_before(c, j0 + jb), cend = c->nloc;  // local trailing cols
         const bool has_next = j + 1 < nblk;
@@ -532,6 +617,9 @@ hpl_status hpl_factor(hpl_ctx *c)
     trace(c, "factor all synced");
     c->launches = t_launches - l0;
     c->factor_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
+    c->h2d_ms = c->h2d_last >= 0 ? ev_ms(c->ev_t[0], c->ev_arr[c->h2d_last]) : 0.0;
+    c->pstart_ms = c->h2d_last >= 0 ? ev_ms(c->ev_t[0], c->ev_t[2]) : 0.0;
+    if (c->h2d_last < 0) c->h2d_bytes = 0;
     c->timeline.clear();
     c->fact_detail.clear();
     c->dgemm_ms = c->laswp_ms = c->trsm_ms = c->fact_ms = 0;
@@ -579,6 +667,38 @@ hpl_status hpl_factor(hpl_ctx *c)
         return HPL_ERR_SINGULAR;
     }
     return HPL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hpl_status hpl_factor(hpl_ctx *c)
+{
+    if (!c) return HPL_ERR_ARG;
+    if (!usable(c, hpl_ctx::S_INIT, "hpl_factor")) {
+        if (c->state != hpl_ctx::S_BROKEN)
+            set_err(c, "hpl_factor: context not in the initialised state");
+        return HPL_ERR_STATE;
+    }
+    return factor_impl(c, nullptr);
+}
+
+hpl_status hpl_load_factor(hpl_ctx *c, const double *host, int64_t ld)
+{
+    if (!c || !host || ld < c->nloc) return HPL_ERR_ARG;
+    if (c->state == hpl_ctx::S_BROKEN) return HPL_ERR_STATE;
+    const int64_t nblk = cdiv(c->N, c->NB);
+    if (c->nranks > 1 || c->nbuf < 4 || nblk < 2) {
+        // (several ranks: their exchanges index 3 panel buffers; load, then factor)
+        ST(hpl_load_local(c, host, ld));
+        return hpl_factor(c);
+    }
+    c->singular = -1;
+    c->state = hpl_ctx::S_INIT;
+    c->loaded = true;
+    const Arrival a{host, ld};
+    return factor_impl(c, &a);
 }
 
 hpl_status hpl_solve(hpl_ctx *c, double *x_host)
@@ -946,9 +1066,14 @@ hpl_status hpl_debug_state(const hpl_ctx *c, uint64_t *out, int64_t cap)
     return HPL_OK;
 }
 
-hpl_status hpl_phase_stats(const hpl_ctx *c, double *out8)
+hpl_status hpl_phase_stats(const hpl_ctx *c, double *out10)   // 12 entries (hpl.h)
 {
-    if (!c || !out8) return HPL_ERR_ARG;
+    if (!c || !out10) return HPL_ERR_ARG;
+    double *out8 = out10;
+    out10[8] = c->h2d_ms;
+    out10[9] = c->h2d_bytes;
+    out10[10] = c->pstart_ms;
+    out10[11] = c->pstart_k;
     out8[0] = c->laswp_ms;
     out8[1] = c->laswp_bytes;
     out8[2] = c->trsm_ms;

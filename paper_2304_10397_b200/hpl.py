@@ -171,6 +171,17 @@ def hpl_load_local(ctx: Ctx, host: np.ndarray) -> None:
     ctx.check(lib.hpl_load_local(ctx.h, ptr(host), cols))
 
 
+def hpl_load_factor(ctx: Ctx, host: np.ndarray) -> None:
+    """hpl_load_local + hpl_factor with the copy overlapped (include/hpl.h);
+    pin `host` with hpl_pin_host for the overlap."""
+    if host.dtype != np.float64 or not host.flags.c_contiguous:
+        raise ValueError("host must be a C-contiguous float64 array")
+    rows, cols = ctx.local_shape
+    if host.shape != (rows, cols):
+        raise ValueError(f"expected local block {(rows, cols)}, got {host.shape}")
+    ctx.check(lib.hpl_load_factor(ctx.h, ptr(host), cols))
+
+
 def hpl_free(ctx: Ctx) -> None:
     if ctx.h is not None and ctx.h.value:
         lib.hpl_free(ctx.h)
@@ -225,10 +236,11 @@ def hpl_last_timing(ctx: Ctx) -> dict:
 
 def hpl_phase_stats(ctx: Ctx) -> dict:
     """Per-phase totals of the last factor/solve (include/hpl.h hpl_phase_stats)."""
-    o = np.zeros(8, dtype=np.float64)
+    o = np.zeros(12, dtype=np.float64)
     ctx.check(lib.hpl_phase_stats(ctx.h, ptr(o)))
     return dict(laswp_ms=o[0], laswp_bytes=o[1], trsm_ms=o[2], trsm_flop=o[3], fact_ms=o[4],
-                solve_ms=o[5], solve_bytes=o[6], dgemm_ms=o[7])
+                solve_ms=o[5], solve_bytes=o[6], dgemm_ms=o[7], h2d_ms=o[8], h2d_bytes=o[9],
+                pipelined_ms=o[10], pipelined_iters=int(o[11]))
 
 
 def hpl_plan_iteration(N: int, NB: int, P: int, Q: int, myrow: int, mycol: int, j: int) -> dict:

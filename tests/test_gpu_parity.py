@@ -448,6 +448,34 @@ def test_load_local_matches_oracle_solve(H):
     assert np.max(np.abs(x - xo)) / np.max(np.abs(xo)) <= 1e-9
 
 
+@pytest.mark.parametrize("N,NB,pinned", [(3000, 128, True), (8192, 256, True), (1024, 256, False),
+                                         (777, 64, True), (8192, 512, True)])
+def test_load_factor_bitwise(H, N, NB, pinned):
+    """hpl_load_factor (copy overlapped with the first iterations, per-chunk
+    streams) gives bitwise the pivots, factors and x of hpl_load_local +
+    hpl_factor on the same host system (the seeded one, read back), and
+    that system's residual is the seeded residual of the same x."""
+    with H.hpl_init(N, NB, 1, 1, 47) as ctx:
+        host = H.hpl_get_local(ctx)
+        if pinned:
+            H.hpl_pin_host(host, True)
+        try:
+            H.hpl_factor(ctx)
+            xa, pa, LUa = H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_get_local(ctx)
+            ra = H.hpl_residual(ctx)
+            H.hpl_load_factor(ctx, host)
+            xb, pb, LUb = H.hpl_solve(ctx), H.hpl_get_ipiv(ctx), H.hpl_get_local(ctx)
+            H.hpl_load_factor(ctx, host)          # twice: streams and events reused
+            xc = H.hpl_solve(ctx)
+        finally:
+            if pinned:
+                H.hpl_pin_host(host, False)
+    assert np.array_equal(pa, pb) and np.array_equal(LUa, LUb)
+    assert np.array_equal(xa, xb) and np.array_equal(xa, xc) and ra < 16
+    o = oracle.run(N, 47)
+    assert np.array_equal(pb, o["ipiv"])
+
+
 def test_hpl_full_size_c2_sampled(H):
     """BASELINE.json configs[2] (N=131072 NB=512, the bench workload, look-ahead
     on): HPL residual < 16 on the device over all rows, and the oracle's own
