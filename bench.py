@@ -240,7 +240,17 @@ def main():
         if rank == 0:
             uid = torch.frombuffer(bytearray(H.hpl_get_unique_id()), dtype=torch.uint8)
         dist.broadcast(uid, 0)
-        ctx = H.hpl_init_dist(N, NB, P, Q, a.seed, rank, world, bytes(uid.tolist()), local)
+        # NCCL may print its version on the process's stdout during init: keep
+        # stdout for the one JSON line (C-level fd 1 -> fd 2 around the init)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            ctx = H.hpl_init_dist(N, NB, P, Q, a.seed, rank, world, bytes(uid.tolist()), local)
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     H.hpl_set_timing(ctx, True)
     peak_meas = H.hplk_dmma_peak()
     cublas_tf = cublas_dgemm_tflops(torch)
