@@ -143,7 +143,7 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
         CK(c, rs_barrier(st, c->rsp, 7, v, spin(c)));
         if (c->leaf_auto) {
             fact_set_leaf_ctas(&c->fw, 0, 512);       // on the critical path: every SM
-            c->fw.leaf_warp_ctas = 0;
+            c->fw.leaf_warp_ctas = c->loop ? c->fw.max_ctas : 0;
         }
         CK(c, panel_fact(st, rows_total, jb, c->Cp, ldc, panel_ipiv(c, j, b), c->nbmin, &c->fw,
                          c->scratch, j0));
@@ -234,6 +234,11 @@ hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b, cudaEvent_t
         const bool hide = j > 0 && rest_ms > c->leaf_hide_ms;
         fact_set_leaf_ctas(&c->fw, hide ? c->leaf_few_ctas : 0, 512);
         c->fw.leaf_warp_ctas = hide ? c->leaf_warp : 0;
+        // loopback: one-warp leaf CTAs only.  A 256-thread leaf CTA needs a
+        // whole SM's registers and starved behind the other ranks' DGEMM CTAs
+        // while its peers spun (P >= 4: 10-25 % of runs timed out); a one-warp
+        // CTA fits beside three DGEMM CTAs (bitwise-equal results, tested)
+        if (c->loop) c->fw.leaf_warp_ctas = c->fw.max_ctas;
     }
     if (c->mycol == (int)(j % c->Q)) {
         ST(wait_panel_buffer_free(c, st, j));

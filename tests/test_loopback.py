@@ -11,7 +11,14 @@ CUDA-IPC mappings.  Checks: identical pivot sequence to the oracle, x within
 1e-9 (BASELINE.json), x / pivots / residual replicated on every rank,
 residual < 16 (SPEC.md l.187-213, l.363 cross-grid consistency).  Each case
 runs in its own process (the loopback needs CUDA_MODULE_LOADING=EAGER and
-32 hardware queues before CUDA initialises) under a timeout."""
+32 hardware queues before CUDA initialises) under a timeout.
+
+The P*Q ranks share one GPU, and their kernels wait on each other: nothing
+guarantees the device co-schedules them (B200_PROFILING.md), and in stress
+runs ~1-3 % of 8-rank runs hit a bounded peer wait (HPL_ERR_PEER) —
+DESIGN.md §6.2 lists what was measured and removed.  A case that ends with
+HPL_ERR_PEER is therefore run once more; a wrong pivot, a wrong x, a CUDA
+error or a second timeout fails."""
 import json
 import os
 import subprocess
@@ -28,10 +35,16 @@ def _run(N, NB, P, Q, *extra, seed=42, expect_ok=True):
                CUDA_DEVICE_MAX_CONNECTIONS="32")
     cmd = [sys.executable, os.path.join(ROOT, "tools", "loop_hpl.py"), str(N), str(NB), str(P),
            str(Q), str(seed), "--oracle", *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
-    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
-    assert lines, r.stdout[-3000:] + r.stderr[-3000:]
-    out = json.loads(lines[-1])
+    for attempt in range(2):
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        assert lines, r.stdout[-3000:] + r.stderr[-3000:]
+        out = json.loads(lines[-1])
+        # one more run only for a co-scheduling timeout of the shared GPU
+        if not (expect_ok and "HPL_ERR_PEER" in out.get("error", "")
+                and "HPL_ERR_CUDA" not in out.get("error", "")):
+            break
+        out["retried_after_peer_timeout"] = True
     if expect_ok:
         assert r.returncode == 0 and out.get("ok", out.get("peer_error_everywhere")), \
             out.get("error", out)
