@@ -633,6 +633,13 @@ hpl_status factor_impl(hpl_ctx *c, const Arrival *arr)
         c->timeline.reserve(6 * nblk);
         c->fact_detail.reserve(3 * nblk);
         for (int64_t j = 0; j < nblk; ++j) {
+            if (j < jstart) {
+                // a pipelined start's iterations ran per chunk without these
+                // events (their records are a previous factorization's)
+                for (int q = 0; q < 6; ++q) c->timeline.push_back(0.0);
+                for (int q = 0; q < 3; ++q) c->fact_detail.push_back(0.0);
+                continue;
+            }
             cudaEvent_t *E = &c->tev[10 * j];
             const double rest_dg = ev_ms(E[2], E[3]);
             c->timeline.push_back(ev_ms(E[5], E[6]));
