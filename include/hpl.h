@@ -134,8 +134,9 @@ hpl_status hpl_regenerate(hpl_ctx *ctx);
 hpl_status hpl_load_local(hpl_ctx *ctx, const double *host, int64_t ld);
 
 /* hpl_load_local + hpl_factor with the host->device copy overlapped with
- * the factorization (one-rank contexts; several ranks fall back to the two
- * calls).  The local block is copied in column chunks on a copy stream and
+ * the factorization (contexts with >= 4 panel buffers, decided at init from
+ * free memory and the same on every rank; otherwise the two calls).  Each
+ * rank passes its own local block.  The local block is copied in column chunks on a copy stream and
  * the updates of the first iterations run per chunk behind the arrivals
  * (DESIGN.md §5 "Pipelined start"), so most of the copy hides behind the
  * DGEMMs; the arithmetic per element is unchanged, the result is bitwise that

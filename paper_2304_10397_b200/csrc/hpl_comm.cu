@@ -76,24 +76,7 @@ hpl_status alloc_ctx(hpl_ctx *c)
     };
     const size_t NBs = (size_t)c->NB;
     if (!M((void **)&c->A, sizeof(double) * (size_t)c->mloc * c->lda)) return HPL_ERR_OOM;
-    c->nbuf = hpl_ctx::NBUF;
-    if (c->nranks == 1) {
-        // one rank: MAXBUF panel states if they leave >= 4 GB free
-        size_t fr = 0, tot = 0;
-        const size_t per = sizeof(double) * ((size_t)c->ldp * (NBs + 1) + (size_t)c->ldlinv * NBs);
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
-            fr > per * hpl_ctx::MAXBUF + 2 * sizeof(double) * NBs * c->ldu + ((size_t)4 << 30))
-            c->nbuf = hpl_ctx::MAXBUF;
-        cudaGetLastError();
-    }
-    for (int b = 0; b < c->nbuf; ++b) {
-        if (!M((void **)&c->panel[b], sizeof(double) * (size_t)c->ldp * (NBs + 1))) return HPL_ERR_OOM;
-        if (!M((void **)&c->linv[b], sizeof(double) * (size_t)c->ldlinv * NBs)) return HPL_ERR_OOM;
-        if (!M((void **)&c->src[b], sizeof(int64_t) * NBs)) return HPL_ERR_OOM;
-        if (!M((void **)&c->disp[b], sizeof(int64_t) * 2 * NBs)) return HPL_ERR_OOM;
-        if (!M((void **)&c->ndisp[b], sizeof(int))) return HPL_ERR_OOM;
-        CK(c, cudaMemset(c->panel[b], 0, sizeof(double) * (size_t)c->ldp * (NBs + 1)));
-    }
+    ST(grow_panels(c, hpl_ctx::NBUF));
     if (!M((void **)&c->gpiv, sizeof(int64_t) * (size_t)c->N)) return HPL_ERR_OOM;
     if (!M((void **)&c->U, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
     if (!M((void **)&c->U2, sizeof(double) * NBs * c->ldu)) return HPL_ERR_OOM;
@@ -161,9 +144,48 @@ hpl_status alloc_ctx(hpl_ctx *c)
     for (cudaEvent_t *e : {&c->ev_rsR, &c->ev_rsL, &c->ev_dgR, &c->ev_dgL, &c->ev_next,
                            &c->ev_rest, &c->ev_trsm})
         CK(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    for (int b = 0; b < c->nbuf; ++b)
-        CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
     for (int k = 0; k < 3; ++k) CK(c, cudaEventCreate(&c->ev_t[k]));
+    // one rank: more panel buffers right away (several ranks agree first)
+    if (c->nranks == 1) ST(grow_panels(c, panels_wanted(c, 1)));
+    return HPL_OK;
+}
+
+int panels_wanted(hpl_ctx *c, int copies)
+{
+    // MAXBUF panel states if they leave >= 4 GB free (copies: contexts on
+    // this device that grow alike — the loopback's ranks)
+    const size_t NBs = (size_t)c->NB;
+    const size_t per = sizeof(double) * ((size_t)c->ldp * (NBs + 1) + (size_t)c->ldlinv * NBs);
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return c->nbuf;
+    }
+    const size_t need = (size_t)copies * per * (size_t)(hpl_ctx::MAXBUF - c->nbuf);
+    return fr > need + ((size_t)4 << 30) ? hpl_ctx::MAXBUF : c->nbuf;
+}
+
+hpl_status grow_panels(hpl_ctx *c, int nbuf)
+{
+    const size_t NBs = (size_t)c->NB;
+    const size_t pbytes = sizeof(double) * (size_t)c->ldp * (NBs + 1);
+    for (int b = 0; b < nbuf; ++b) {
+        if (c->panel[b]) continue;
+        bool ok = cudaMalloc((void **)&c->panel[b], pbytes) == cudaSuccess &&
+                  cudaMalloc((void **)&c->linv[b], sizeof(double) * (size_t)c->ldlinv * NBs) ==
+                      cudaSuccess &&
+                  cudaMalloc((void **)&c->src[b], sizeof(int64_t) * NBs) == cudaSuccess &&
+                  cudaMalloc((void **)&c->disp[b], sizeof(int64_t) * 2 * NBs) == cudaSuccess &&
+                  cudaMalloc((void **)&c->ndisp[b], sizeof(int)) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            set_err(c, "cudaMalloc of panel buffer %d failed", b);
+            return HPL_ERR_OOM;
+        }
+        CK(c, cudaMemset(c->panel[b], 0, pbytes));
+        CK(c, cudaEventCreateWithFlags(&c->ev_panel[b], cudaEventDisableTiming));
+    }
+    c->nbuf = std::max(c->nbuf, nbuf);
     return HPL_OK;
 }
 
@@ -173,7 +195,7 @@ PeerExports exports_of(const hpl_ctx *c)
     e.A = c->A;
     e.xbuf = c->xbuf;
     e.rsflag = c->rsflag;
-    for (int b = 0; b < 3; ++b) e.panel[b] = c->panel[b];
+    for (int b = 0; b < c->nbuf; ++b) e.panel[b] = c->panel[b];
     e.lbflag = c->lbflag;
     e.cb = c->cb;
     return e;
@@ -181,7 +203,7 @@ PeerExports exports_of(const hpl_ctx *c)
 
 hpl_status setup_peers(hpl_ctx *c, const std::vector<PeerExports> &ex)
 {
-    const int P = c->P, Q = c->Q, NBUF = hpl_ctx::NBUF;
+    const int P = c->P, Q = c->Q, MB = hpl_ctx::MAXBUF;
     if ((int)ex.size() != c->nranks) return HPL_ERR_ARG;
     if (P > 1) {
         c->rsp.P = P;
@@ -195,7 +217,7 @@ hpl_status setup_peers(hpl_ctx *c, const std::vector<PeerExports> &ex)
             const PeerExports &e = ex[p + c->mycol * P];
             c->rsp.A[p] = e.A;
             c->rsp.flag[p] = e.rsflag;
-            for (int b = 0; b < 3; ++b) c->colpanel[p][b] = e.panel[b];
+            for (int b = 0; b < MB; ++b) c->colpanel[p][b] = e.panel[b];
             c->xch.rec[p] = static_cast<double *>(e.xbuf);
             c->xch.flag[p] = reinterpret_cast<unsigned long long *>(static_cast<char *>(e.xbuf) +
                                                                     rec_bytes);
@@ -204,11 +226,11 @@ hpl_status setup_peers(hpl_ctx *c, const std::vector<PeerExports> &ex)
         c->xch.my_flag = c->xch.flag[c->myrow];
     }
     if (Q > 1) {
-        c->ppanel.assign((size_t)Q * NBUF, nullptr);
+        c->ppanel.assign((size_t)Q * MB, nullptr);
         c->pflag.assign(Q, nullptr);
         for (int q = 0; q < Q; ++q) {
             const PeerExports &e = ex[c->myrow + q * P];
-            for (int b = 0; b < NBUF; ++b) c->ppanel[(size_t)q * NBUF + b] = e.panel[b];
+            for (int b = 0; b < MB; ++b) c->ppanel[(size_t)q * MB + b] = e.panel[b];
             c->pflag[q] = e.lbflag;
         }
     }
@@ -362,7 +384,8 @@ namespace {
 // all-gather over the world at init); a rank maps what its exchanges read —
 // the process column's A, RS flags, pivot-exchange areas and packed panels,
 // the process row's panel buffers and LBCAST flags, everyone's comm block.
-constexpr int NH = 8;   // A, xbuf, rsflag, panel 0..2, lbflag, cb
+constexpr int HP = 3;                   // handle index of panel[0]
+constexpr int NH = HP + MAX_PANELS + 2;  // A, xbuf, rsflag, panel[0..MAX_PANELS), lbflag, cb
 struct Handles {
     cudaIpcMemHandle_t h[NH];
     int have[NH];
@@ -371,8 +394,10 @@ struct Handles {
 hpl_status exchange_ipc(hpl_ctx *c, std::vector<PeerExports> *out)
 {
     const PeerExports me = exports_of(c);
-    void *ptrs[NH] = {me.A, me.xbuf, me.rsflag, me.panel[0], me.panel[1], me.panel[2],
-                      me.lbflag, me.cb};
+    void *ptrs[NH] = {me.A, me.xbuf, me.rsflag};
+    for (int b = 0; b < MAX_PANELS; ++b) ptrs[HP + b] = me.panel[b];
+    ptrs[HP + MAX_PANELS] = me.lbflag;
+    ptrs[HP + MAX_PANELS + 1] = me.cb;
     Handles mine{};
     for (int k = 0; k < NH; ++k) {
         mine.have[k] = ptrs[k] != nullptr;
@@ -411,12 +436,14 @@ hpl_status exchange_ipc(hpl_ctx *c, std::vector<PeerExports> *out)
             if (!e.A || !e.xbuf || !e.rsflag) goto fail;
         }
         if (same_col || same_row) {
-            for (int b = 0; b < 3; ++b)
-                if (!(e.panel[b] = static_cast<double *>(open(3 + b)))) goto fail;
+            // every rank holds the same nbuf buffers (agreed at init)
+            for (int b = 0; b < c->nbuf; ++b)
+                if (!(e.panel[b] = static_cast<double *>(open(HP + b)))) goto fail;
         }
-        if (same_row && c->Q > 1 && !(e.lbflag = static_cast<unsigned long long *>(open(6))))
+        if (same_row && c->Q > 1 &&
+            !(e.lbflag = static_cast<unsigned long long *>(open(HP + MAX_PANELS))))
             goto fail;
-        if (!(e.cb = static_cast<CommBlock *>(open(7)))) goto fail;
+        if (!(e.cb = static_cast<CommBlock *>(open(HP + MAX_PANELS + 1)))) goto fail;
         continue;
     fail:
         set_err(c, "cudaIpcOpenMemHandle of rank %d's buffers failed (ranks must share one node "
@@ -481,6 +508,17 @@ hpl_status hpl_init_dist(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64_t s
     NK(c, ncclCommSplit(c->world_nccl, c->mycol, c->myrow, &c->g[G_COL].nccl, nullptr));
     NK(c, ncclCommSplit(c->world_nccl, c->mycol, c->myrow, &c->g[G_COLTR].nccl, nullptr));
     ST(alloc_ctx(c));
+    if (nranks > 1) {
+        // the same number of panel buffers on every rank: the minimum wanted
+        const int32_t want = panels_wanted(c, 1);
+        int32_t *d = reinterpret_cast<int32_t *>(c->out4);
+        CK(c, cudaMemcpy(d, &want, sizeof want, cudaMemcpyHostToDevice));
+        NK(c, ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c->world_nccl, c->s_la));
+        int32_t agreed = 0;
+        CK(c, cudaMemcpyAsync(&agreed, d, sizeof agreed, cudaMemcpyDeviceToHost, c->s_la));
+        CK(c, cudaStreamSynchronize(c->s_la));
+        ST(grow_panels(c, agreed));
+    }
     std::vector<PeerExports> ex;
     if (nranks > 1) ST(exchange_ipc(c, &ex));
     else ex.assign(1, exports_of(c));
@@ -516,6 +554,11 @@ hpl_status hpl_init_loopback(int64_t N, int32_t NB, int32_t P, int32_t Q, uint64
         c->dist = nr > 1;
         c->loop = true;
         s = alloc_ctx(c);
+    }
+    if (s == HPL_OK && nr > 1) {
+        // the ranks share this device: they all grow, or none does
+        const int want = panels_wanted(cs[0], nr);
+        for (int r = 0; r < nr && s == HPL_OK; ++r) s = grow_panels(cs[r], want);
     }
     std::vector<PeerExports> ex(nr);
     for (int r = 0; r < nr && s == HPL_OK; ++r) ex[r] = exports_of(cs[r]);

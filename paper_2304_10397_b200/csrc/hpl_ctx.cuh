@@ -23,13 +23,16 @@ struct Group {
     GroupDev dev{};
 };
 
+// Panel buffers a context can hold (hpl_ctx::nbuf of them in use).
+constexpr int MAX_PANELS = 8;
+
 // Device pointers one rank shares with its peers (IPC handles in a
 // multi-process grid, plain pointers in the single-device loopback).
 struct PeerExports {
     double *A = nullptr;
     void *xbuf = nullptr;
     unsigned long long *rsflag = nullptr;
-    double *panel[3] = {nullptr, nullptr, nullptr};
+    double *panel[MAX_PANELS] = {};          // panel[b], b < nbuf (null beyond)
     unsigned long long *lbflag = nullptr;
     CommBlock *cb = nullptr;
 };
@@ -62,7 +65,7 @@ struct hpl_ctx {
     hpl::RsPeers rsp{};
     unsigned long long rs_seq[3] = {0, 0, 0};
     // P > 1 gathered panel FACT for small panels
-    const double *colpanel[hpl::MAX_P][3] = {};
+    const double *colpanel[hpl::MAX_P][hpl::MAX_PANELS] = {};
     double *Cp = nullptr;            // combined panel, cp_max_rows x NB (col-major)
     int64_t cp_max_rows = 0;
     int64_t fact_gather_rows = 65536;
@@ -75,18 +78,19 @@ struct hpl_ctx {
     bool lb_peer = true;
     unsigned long long lb_base = 0, lb_next = 0;
     unsigned long long *lbflag = nullptr;
-    std::vector<const double *> ppanel;         // [q * NBUF + b]: column q's panel[b]
+    std::vector<const double *> ppanel;         // [q * MAXBUF + b]: column q's panel[b]
     std::vector<unsigned long long *> pflag;    // [q]: column q's lbflag
     double *rvec = nullptr, *avec = nullptr, *bvec = nullptr;   // residual partial sums
     // local storage
     int64_t mloc = 0, nloc = 0, lda = 0;
     double *A = nullptr;
     // per-panel state (panel, L11^{-1}, pivot plan): panels j, j+1, j+2 are
-    // live at once in the look-ahead loop.  NBUF = 3 buffers where peers index
-    // them (P*Q > 1: the LBCAST pull and the gathered FACT read buffer j mod 3);
-    // a one-rank context keeps MAXBUF (memory permitting) so hpl_load_factor's
-    // pipelined start can have K + 1 panels in flight (nbuf = buffers in use).
-    static constexpr int NBUF = 3, MAXBUF = 8;
+    // live at once in the look-ahead loop, so NBUF = 3 buffers suffice; a
+    // context keeps MAXBUF (memory permitting) so hpl_load_factor's pipelined
+    // start can have K + 1 panels in flight.  nbuf = buffers in use, the same
+    // on every rank of a grid (peers index each other's buffer j mod nbuf:
+    // the LBCAST pull, the gathered FACT).
+    static constexpr int NBUF = 3, MAXBUF = hpl::MAX_PANELS;
     int nbuf = NBUF;
     double *panel[MAXBUF] = {};
     int64_t ldp = 0;
@@ -198,6 +202,10 @@ inline int64_t numroc(int64_t n, int nb, int me, int nprocs)
 // ---- hpl_comm.cu
 // Allocate the context's device memory, streams and events (P, Q, rank set).
 hpl_status alloc_ctx(hpl_ctx *c);
+// Panel buffers: how many this device can hold for `copies` contexts, and
+// allocate buffers [nbuf, n).
+int panels_wanted(hpl_ctx *c, int copies);
+hpl_status grow_panels(hpl_ctx *c, int n);
 // Wire the peer tables (RS, pivot exchange, gathered FACT, LBCAST, groups)
 // from every rank's exports (world-indexed, this process's address space).
 hpl_status setup_peers(hpl_ctx *c, const std::vector<PeerExports> &ex);

@@ -163,15 +163,15 @@ hpl_status fact_local(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
     return HPL_OK;
 }
 
-// Panel j is about to be written into this rank's panel[j % NBUF] (by FACT on
+// Panel j is about to be written into this rank's panel[j % nbuf] (by FACT on
 // the owner, by the LBCAST copy elsewhere).  If this rank owned panel
-// j - NBUF, the other columns may still be pulling it from that buffer: wait
+// j - nbuf, the other columns may still be pulling it from that buffer: wait
 // until every one of them has copied it (their done words in this rank's
-// lbflag).  Owners of j - NBUF are the only ranks whose buffer peers read.
+// lbflag).  Owners of j - nbuf are the only ranks whose buffer peers read.
 hpl_status wait_panel_buffer_free(hpl_ctx *c, cudaStream_t st, int64_t j)
 {
-    if (c->Q == 1 || !c->lb_peer || j < hpl_ctx::NBUF) return HPL_OK;
-    const int64_t jo = j - hpl_ctx::NBUF;
+    if (c->Q == 1 || !c->lb_peer || j < c->nbuf) return HPL_OK;
+    const int64_t jo = j - c->nbuf;
     if ((int)(jo % c->Q) != c->mycol) return HPL_OK;
     FlagOp op{};
     for (int q = 0; q < c->Q; ++q)
@@ -202,7 +202,7 @@ hpl_status lbcast_and_plan(hpl_ctx *c, cudaStream_t st, int64_t j, int b)
             op.wt[op.nwait++] = c->lbflag + pcol;
             op.wv = c->lb_base + (unsigned long long)j + 1;
             CK(c, flag_op(st, op, spin(c)));
-            ST(d2d(c, st, c->panel[b], c->ppanel[pcol * hpl_ctx::NBUF + b], pbytes));
+            ST(d2d(c, st, c->panel[b], c->ppanel[pcol * hpl_ctx::MAXBUF + b], pbytes));
             FlagOp done{};
             done.sig[done.nsig++] = c->pflag[pcol] + hpl_ctx::LB_DONE + c->mycol;
             done.sv = c->lb_base + (unsigned long long)j + 1;
@@ -388,7 +388,7 @@ struct Arrival {
     int64_t ld;
 };
 
-// Pipelined start (hpl_load_factor, one rank): the local matrix is copied in
+// Pipelined start (hpl_load_factor): the local matrix is copied in
 // column chunks (whole NB blocks) on a copy stream while the first K
 // iterations run chunk by chunk, in chunk-major order on S_la: chunk 0 —
 // which holds panels 0..K — is factored and updated first (FACT(j+1) right
@@ -400,6 +400,12 @@ struct Arrival {
 // ran every chunk on its own stream: the FACT chain's kernels, which need
 // whole SMs, starved behind the stream of DGEMM CTAs — FACT(1) ready at
 // 0.23 s finished at 1.59 s — DESIGN.md §5.)  On return FACT(K) is done.
+// Several ranks: every rank runs the same sequence on its local columns —
+// FACT/LBCAST(0..K) all in chunk 0 (chunk 0 holds panels 0..K's local
+// columns on every process column), then per chunk the K updates, whose RS
+// barriers pair up within a process column (same nloc, so the same chunks);
+// a rank signals an RS barrier only after its own chunk has landed, so the
+// peer rows it gathers are in place.  K and nbuf are the same on every rank.
 hpl_status pipelined_start(hpl_ctx *c, const Arrival &a, int64_t *jstart)
 {
     const int64_t nblk = cdiv(c->N, c->NB);
@@ -442,7 +448,7 @@ hpl_status pipelined_start(hpl_ctx *c, const Arrival &a, int64_t *jstart)
     // GPU, so the leaf gets every SM
     c->leaf_auto = false;
     fact_set_leaf_ctas(&c->fw, 0, 512);
-    c->fw.leaf_warp_ctas = 0;
+    c->fw.leaf_warp_ctas = c->loop ? c->fw.max_ctas : 0;   // loopback: fact_panel
     CK(c, cudaStreamWaitEvent(st, c->ev_arr[0], 0));
     ST(fact_panel(c, st, 0, 0));
     for (int64_t j = 0; j < K; ++j) {
@@ -701,8 +707,9 @@ hpl_status hpl_load_factor(hpl_ctx *c, const double *host, int64_t ld)
     if (!c || !host || ld < c->nloc) return HPL_ERR_ARG;
     if (c->state == hpl_ctx::S_BROKEN) return HPL_ERR_STATE;
     const int64_t nblk = cdiv(c->N, c->NB);
-    if (c->nranks > 1 || c->nbuf < 4 || nblk < 2) {
-        // (several ranks: their exchanges index 3 panel buffers; load, then factor)
+    if (c->nbuf < 4 || nblk < 2) {
+        // (too few panel buffers for K >= 3 panels in flight: load, then
+        // factor; nbuf is the same on every rank of a grid)
         ST(hpl_load_local(c, host, ld));
         return hpl_factor(c);
     }

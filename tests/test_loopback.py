@@ -124,3 +124,21 @@ def test_loopback_absent_rank_times_out():
     out = _run(1024, 64, 2, 2, "--absent", "3", "--timeout-ms", "2000")
     assert out["peer_error_everywhere"] and out["statuses"] == [7, 7, 7], out
     assert out["wall_s"] < 60
+
+
+@pytest.mark.parametrize("P,Q,extra", [(1, 2, ()), (2, 1, ()), (2, 2, ()), (2, 4, ()),
+                                       (2, 2, ("--opt=split=30",)),
+                                       (2, 2, ("--opt=rs_peer=0", "--opt=lb_peer=0")),
+                                       (2, 2, ("--opt=fact_gather=1048576",
+                                               "--opt=fact_gather_ms=100000"))])
+def test_loopback_load_factor_bitwise(P, Q, extra):
+    """hpl_load_factor on a grid (the pipelined start: every rank copies its
+    local block in column chunks while the first K iterations run chunk by
+    chunk, FACT/LBCAST of panels 0..K in chunk 0, per-chunk RS barriers
+    within the process column): pivots, factors and x bitwise those of
+    hpl_load_local + hpl_factor on every rank; then the seeded system again
+    vs the oracle."""
+    out = _run(3000, 64, P, Q, "--load-factor", *extra)
+    _check(out)
+    assert out["load_factor_bitwise"], out
+    assert all(k == 6 for k in out["pipelined_iters"]), out

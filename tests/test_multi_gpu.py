@@ -137,6 +137,19 @@ def test_peer_exchange_vs_nccl(P, Q, split):
         assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16, (v, out)
 
 
+@pytest.mark.parametrize("P,Q", [(1, 2), (2, 1), (2, 2)])
+def test_load_factor_multi_gpu_bitwise(P, Q):
+    """hpl_load_factor across processes (each rank copies its local block in
+    column chunks while the first iterations run chunk by chunk; CUDA-IPC
+    panel buffers agreed at init): bitwise the LU, pivots and x of
+    hpl_load_local + hpl_factor on every rank."""
+    if _ngpu() < P * Q:
+        pytest.skip(f"needs {P * Q} GPUs")
+    out = _run(P * Q, 3000, 64, P, Q, ("--load-factor",))
+    assert out["load_factor_bitwise"], out
+    assert out["ipiv_equal"] and out["x_rel"] <= 1e-9 and out["resid"] < 16, out
+
+
 def test_rank_death_gives_peer_error():
     """SPEC.md l.191 / l.360: rank 1 exits 300 ms into hpl_factor; rank 0's
     bounded peer waits end its call with HPL_ERR_PEER instead of a hang.

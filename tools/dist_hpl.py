@@ -2,11 +2,13 @@
 
     torchrun --nproc-per-node Q --master-addr 127.0.0.1 --master-port PORT \\
         tools/dist_hpl.py N NB P Q [seed] [--oracle] [--la 0|1] [--repeat K] [--opt=k=v]
-        [--die RANK:MS] [--timeout-ms T]
+        [--die RANK:MS] [--timeout-ms T] [--load-factor]
 
 rank 0 creates the NCCL unique id (hpl_get_unique_id); it travels to the other
 ranks over a gloo process group; every rank then calls hpl_init_dist.  With
 --oracle, rank 0 compares the pivots and x with the CPU oracle.
+--load-factor: every rank then runs hpl_load_factor (pipelined start) on its
+original local block; LU, pivots and x must equal the first run's bitwise.
 Prints one JSON line on rank 0; exit code 0 iff residual < 16 (and parity).
 """
 import json
@@ -102,6 +104,23 @@ def main():
                            fmt="%.4f", header="fact,la_update,rest_update,rest_rs,rest_trsm,"
                            "rest_dgemm,fact_wait,fact_local,lbcast_plan")
     ipiv = H.hpl_get_ipiv(ctx)
+    lf_ok = True
+    if "--load-factor" in sys.argv:
+        # the pipelined start (copy overlapped with the first iterations) on
+        # this rank's original local block: bitwise the same LU, pivots and x
+        LU = H.hpl_get_local(ctx)
+        H.hpl_regenerate(ctx)
+        host = H.hpl_get_local(ctx)
+        H.hpl_pin_host(host, True)
+        H.hpl_load_factor(ctx, host)
+        xb = H.hpl_solve(ctx)
+        H.hpl_pin_host(host, False)
+        lf_ok = bool(np.array_equal(x, xb) and np.array_equal(ipiv, H.hpl_get_ipiv(ctx)) and
+                     np.array_equal(LU, H.hpl_get_local(ctx)) and
+                     H.hpl_phase_stats(ctx)["pipelined_iters"] > 0)
+        H.hpl_regenerate(ctx)         # the seeded system again, for the residual
+        H.hpl_factor(ctx)
+        H.hpl_solve(ctx, want_x=False)
     r = H.hpl_residual(ctx)
     H.hpl_free(ctx)
     dev = torch.tensor([tm["factor_ms"] + tm["solve_ms"]], dtype=torch.float64)
@@ -125,6 +144,11 @@ def main():
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     out["x_replicated"] = bool(flag.item())
     ok = ok and out["x_replicated"]
+    if "--load-factor" in sys.argv:
+        f2 = torch.tensor([1 if lf_ok else 0], dtype=torch.int64)
+        dist.all_reduce(f2, op=dist.ReduceOp.MIN)
+        out["load_factor_bitwise"] = bool(f2.item())
+        ok = ok and out["load_factor_bitwise"]
     if rank == 0:
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()

@@ -2,7 +2,7 @@
 host thread per rank) through the C ABI — hpl_init_loopback, include/hpl.h.
 
     python tools/loop_hpl.py N NB P Q [seed] [--oracle] [--la 0|1] [--repeat K]
-        [--opt=k=v ...] [--tie] [--absent RANK] [--timeout-ms T]
+        [--opt=k=v ...] [--tie] [--absent RANK] [--timeout-ms T] [--load-factor]
 
 Every rank runs the multi-GPU data path (peer-memory RS, pivot exchange,
 LBCAST flags, collectives) on the same device, so a 1-GPU box checks rows
@@ -12,6 +12,10 @@ panel has exact pivot ties between rows of different process rows
 (hpl_inputs.twin_system) and compares with the oracle's GEPP of it.
 --absent R: rank R never calls hpl_factor; every other rank must get
 HPL_ERR_PEER (bounded waits) instead of hanging.
+--load-factor: afterwards every rank runs hpl_load_factor (the pipelined
+start: copy overlapped with the first iterations) on its original local
+block from pinned host memory; pivots, factors and x must equal the first
+run's bitwise.
 Prints one JSON line; exit code 0 iff every check passed.
 """
 import json
@@ -96,13 +100,35 @@ def main():
             H.run_ranks(lambda c: (load(c), H.hpl_factor(c), H.hpl_solve(c, want_x=False),
                                    H.hpl_regenerate(c)), ctxs)
         H.run_ranks(load, ctxs)
+        lf = "--load-factor" in flags
+        hosts = [H.hpl_get_local(c) for c in ctxs] if lf else None
         t0 = time.perf_counter()
         xs = H.run_ranks(lambda c: (H.hpl_factor(c), H.hpl_solve(c))[1], ctxs)
         out["wall_s"] = time.perf_counter() - t0
         ipivs = [H.hpl_get_ipiv(c) for c in ctxs]
+        if lf:
+            LUs = [H.hpl_get_local(c) for c in ctxs]
+            for h in hosts:
+                H.hpl_pin_host(h, True)
+            try:
+                xb = H.run_ranks(lambda c: (H.hpl_load_factor(c, hosts[ctxs.index(c)]),
+                                            H.hpl_solve(c))[1], ctxs)
+            finally:
+                for h in hosts:
+                    H.hpl_pin_host(h, False)
+            out["load_factor_bitwise"] = bool(
+                all(np.array_equal(a, b) for a, b in zip(xs, xb)) and
+                all(np.array_equal(p, H.hpl_get_ipiv(c)) for p, c in zip(ipivs, ctxs)) and
+                all(np.array_equal(L, H.hpl_get_local(c)) for L, c in zip(LUs, ctxs)))
+            out["pipelined_iters"] = [H.hpl_phase_stats(c).get("pipelined_iters")
+                                      for c in ctxs]
+            ok = out["load_factor_bitwise"]
+            # the loaded system has no seeded residual (HPL_ERR_STATE): back to it
+            H.run_ranks(H.hpl_regenerate, ctxs)
+            xs = H.run_ranks(lambda c: (H.hpl_factor(c), H.hpl_solve(c))[1], ctxs)
         out["ipiv_replicated"] = all(np.array_equal(ipivs[0], p) for p in ipivs)
         out["x_replicated"] = all(np.array_equal(xs[0], x) for x in xs)
-        ok = out["ipiv_replicated"] and out["x_replicated"]
+        ok = ok and out["ipiv_replicated"] and out["x_replicated"]
         x, ipiv = xs[0], ipivs[0]
         if not tie:
             rs = H.run_ranks(H.hpl_residual, ctxs)
