@@ -6,8 +6,11 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/fp64p tools/fp64_pipes.cu
 //   /tmp/fp64p
+// Also: the DGEMM consumer loop fed from shared memory (no TMA, no
+// epilogue), with and without a register double buffer of the fragments.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdint>
 
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0)
 {
@@ -49,6 +52,99 @@ __global__ void __launch_bounds__((WM + WF) * 32) pipes(int iters, double *out)
     if (s == 12345.678) out[0] = s;
 }
 
+// The DGEMM consumer warp's inner loop (kernels_gemm.cu, CfgC 32x32 warp
+// tile): per k-step 2 A + 2 B fragments by ld.shared.v2.f64 from a swizzled
+// 128-B-row stage, then 8 m16n8k4 DMMAs; PREF=1 loads the next k-step's
+// fragments before the current DMMAs (register double buffer).
+__device__ __forceinline__ double2 lds128(uint32_t addr)
+{
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+template <int PREF>
+__global__ void __launch_bounds__(128, 3) ldsfed(int iters, double *out)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    for (int i = threadIdx.x; i < 8192; i += blockDim.x)
+        reinterpret_cast<double *>(sm)[i] = 1e-9 * i;
+    __syncthreads();
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, w = threadIdx.x >> 5;
+    const uint32_t sA = base + (w & 1) * 2 * 2048, sB = base + 16384 + (w >> 1) * 2 * 2048;
+    double acc[2][2][2][4] = {};
+    auto offs = [&](int ks) {
+        const int kr = 8 * (ks >> 1) + (ks & 1) + 2 * t;
+        return (uint32_t)(kr * 128 + ((g ^ (kr & 7)) << 4));
+    };
+    for (int it = 0; it < iters; ++it) {
+        if (PREF) {
+            double2 a[2], b[2], an[2], bn[2];
+            uint32_t off = offs(0);
+            for (int i = 0; i < 2; ++i) a[i] = lds128(sA + i * 2048 + off);
+            for (int j = 0; j < 2; ++j) b[j] = lds128(sB + j * 2048 + off);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                if (ks < 3) {
+                    off = offs(ks + 1);
+                    for (int i = 0; i < 2; ++i) an[i] = lds128(sA + i * 2048 + off);
+                    for (int j = 0; j < 2; ++j) bn[j] = lds128(sB + j * 2048 + off);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        dmma(acc[i][j][0], a[i].x, a[i].y, b[j].x);
+                        dmma(acc[i][j][1], a[i].x, a[i].y, b[j].y);
+                    }
+                for (int i = 0; i < 2; ++i) { a[i] = an[i]; b[i] = bn[i]; }
+            }
+        } else {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint32_t off = offs(ks);
+                double2 a[2], b[2];
+                for (int i = 0; i < 2; ++i) a[i] = lds128(sA + i * 2048 + off);
+                for (int j = 0; j < 2; ++j) b[j] = lds128(sB + j * 2048 + off);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        dmma(acc[i][j][0], a[i].x, a[i].y, b[j].x);
+                        dmma(acc[i][j][1], a[i].x, a[i].y, b[j].y);
+                    }
+            }
+        }
+    }
+    double s = 0;
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
+            for (int h = 0; h < 2; ++h)
+                for (int c = 0; c < 4; ++c) s += acc[i][j][h][c];
+    if (s == 12345.678) out[0] = s;
+}
+
+template <int PREF>
+void run_lds(const char *name, int blocks_per_sm, int sms, int iters, double *out)
+{
+    cudaFuncSetAttribute(ldsfed<PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = sms * blocks_per_sm;
+    ldsfed<PREF><<<grid, 128, 65536>>>(iters, out);
+    cudaEventRecord(e0);
+    ldsfed<PREF><<<grid, 128, 65536>>>(iters, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flop = 1024.0 * 32 * (double)iters * 4 * grid;
+    printf("%-28s blocks/SM %d: %.2f TF/s (%.2f ms) %s\n", name, blocks_per_sm, flop / ms / 1e9, ms,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int WM, int WF>
 void run(const char *name, int blocks_per_sm, int sms, int iters, double *out)
 {
@@ -84,5 +180,9 @@ int main()
     run<8, 4>("DMMA 8 + DFMA 4 warps", 2, sms, it, out);
     run<12, 4>("DMMA 12 + DFMA 4 warps", 1, sms, it, out);
     run<4, 4>("DMMA 4 + DFMA 4 warps", 2, sms, it, out);
+    run<4, 0>("DMMA only (4 warps)", 3, sms, it, out);
+    run<4, 0>("DMMA only (4 warps)", 2, sms, it, out);
+    run_lds<0>("LDS-fed 4 warps", 3, sms, it / 4, out);
+    run_lds<1>("LDS-fed 4 warps, prefetch", 3, sms, it / 4, out);
     return 0;
 }
