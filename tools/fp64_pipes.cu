@@ -64,10 +64,10 @@ __device__ __forceinline__ double2 lds128(uint32_t addr)
 }
 
 template <int PREF>
-__global__ void __launch_bounds__(128, 3) ldsfed(int iters, double *out)
+__global__ void __launch_bounds__(128, 4) ldsfed(int iters, double *out)
 {
     extern __shared__ __align__(1024) unsigned char sm[];
-    for (int i = threadIdx.x; i < 8192; i += blockDim.x)
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
         reinterpret_cast<double *>(sm)[i] = 1e-9 * i;
     __syncthreads();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
@@ -128,14 +128,14 @@ __global__ void __launch_bounds__(128, 3) ldsfed(int iters, double *out)
 template <int PREF>
 void run_lds(const char *name, int blocks_per_sm, int sms, int iters, double *out)
 {
-    cudaFuncSetAttribute(ldsfed<PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaFuncSetAttribute(ldsfed<PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int grid = sms * blocks_per_sm;
-    ldsfed<PREF><<<grid, 128, 65536>>>(iters, out);
+    ldsfed<PREF><<<grid, 128, 32768>>>(iters, out);
     cudaEventRecord(e0);
-    ldsfed<PREF><<<grid, 128, 65536>>>(iters, out);
+    ldsfed<PREF><<<grid, 128, 32768>>>(iters, out);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -184,5 +184,7 @@ int main()
     run<4, 0>("DMMA only (4 warps)", 2, sms, it, out);
     run_lds<0>("LDS-fed 4 warps", 3, sms, it / 4, out);
     run_lds<1>("LDS-fed 4 warps, prefetch", 3, sms, it / 4, out);
+    run_lds<0>("LDS-fed 4 warps", 4, sms, it / 4, out);
+    run_lds<1>("LDS-fed 4 warps, prefetch", 4, sms, it / 4, out);
     return 0;
 }
