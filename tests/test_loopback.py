@@ -142,3 +142,14 @@ def test_loopback_load_factor_bitwise(P, Q, extra):
     _check(out)
     assert out["load_factor_bitwise"], out
     assert all(k == 6 for k in out["pipelined_iters"]), out
+
+
+@pytest.mark.parametrize("N,NB,P,Q", [(100, 64, 2, 4), (64, 64, 2, 2), (130, 64, 4, 1), (2, 2, 1, 2),
+                                      (33, 32, 2, 2), (66, 32, 2, 4), (200, 64, 1, 4),
+                                      (129, 64, 2, 1), (513, 64, 4, 2), (4, 2, 2, 2)])
+def test_loopback_degenerate_grids(N, NB, P, Q):
+    """Grids where some ranks own no matrix rows or no columns (N=100 on 2x4:
+    process columns 2 and 3 hold nothing; N=NB: one block; ragged last
+    blocks of 1-2 rows/columns; N=2 and 4): every rank still takes part in
+    every collective and the result is the oracle's."""
+    _check(_run(N, NB, P, Q))
