@@ -8,7 +8,7 @@ import sys
 def short_name(name: str) -> str:
     if "dgemm_tma_kernel" in name:
         m = re.search(r"Cfg<(\d+), (\d+), \d+, \d+, \d+, \d+>, (\d)", name)
-        role = {"0": "trailing", "1": "look-ahead", "2": "FACT recursion"}
+        role = {"0": "trailing", "1": "look-ahead", "2": "FACT recursion", "3": "DTRSM, RS stream"}
         if m:
             return f"dgemm_tma_kernel<{m.group(1)}x{m.group(2)}> ({role.get(m.group(3), m.group(3))})"
     s = re.sub(r"\(.*", "", name)
