@@ -388,33 +388,38 @@ struct Arrival {
     int64_t ld;
 };
 
-// Pipelined start (hpl_load_factor): the local matrix is copied in
-// column chunks (whole NB blocks) on a copy stream while the first K
-// iterations run chunk by chunk, in chunk-major order on S_la: chunk 0 —
-// which holds panels 0..K — is factored and updated first (FACT(j+1) right
-// after update(j) of chunk 0, each with the whole GPU), then every later chunk
-// receives its K updates as soon as it has landed.  Per column the same
-// kernels run in the same order as in the look-ahead loop, so the result is
-// bitwise that of hpl_load_local + hpl_factor (tested); the copy of the
-// later chunks hides behind the earlier chunks' updates.  (A first version
-// ran every chunk on its own stream: the FACT chain's kernels, which need
-// whole SMs, starved behind the stream of DGEMM CTAs — FACT(1) ready at
-// 0.23 s finished at 1.59 s — DESIGN.md §5.)  On return FACT(K) is done.
-// Several ranks: every rank runs the same sequence on its local columns —
-// FACT/LBCAST(0..K) all in chunk 0 (chunk 0 holds panels 0..K's local
-// columns on every process column), then per chunk the K updates, whose RS
-// barriers pair up within a process column (same nloc, so the same chunks);
-// a rank signals an RS barrier only after its own chunk has landed, so the
-// peer rows it gathers are in place.  K and nbuf are the same on every rank.
+// Pipelined start (hpl_load_factor): the local matrix is copied in column
+// chunks (whole NB blocks) on a copy stream while the first K iterations run
+// chunk by chunk on S_la.  The first K+1 chunks are one local block each, so
+// FACT(0) starts after one block has landed and FACT(j) follows as soon as
+// the block holding panel j has received updates 0..j-1; the later chunks,
+// growing from 2 to 16 blocks, receive their K updates each as they land.  Per
+// column the same kernels run in the same order as in the look-ahead loop,
+// so the result is bitwise that of hpl_load_local + hpl_factor (tested); the
+// copy of the later chunks hides behind the earlier chunks' updates.  (A
+// first version ran every chunk on its own stream: the FACT chain's kernels,
+// which need whole SMs, starved behind the stream of DGEMM CTAs; a second
+// one used 16 equal chunks, chunk 0 holding panels 0..K: 8.6 GB landed
+// before FACT(0) could start — DESIGN.md §5.)  On return FACT(K) is done.
+// Several ranks: every rank runs FACT/LBCAST(0..K) in order; the updates a
+// rank applies depend only on its process column (same nloc, hence the same
+// chunks), so the RS barriers pair up within a process column; a rank
+// signals an RS barrier only after its own chunk has landed, so the peer rows
+// it gathers are in place.  K and nbuf are the same on every rank.
 hpl_status pipelined_start(hpl_ctx *c, const Arrival &a, int64_t *jstart)
 {
     const int64_t nblk = cdiv(c->N, c->NB);
     const int K = (int)std::min<int64_t>(std::min<int64_t>(6, c->nbuf - 1), nblk - 1);
     const int64_t nbl_cols = cdiv(c->nloc, c->NB);            // local column blocks (b included)
-    // chunk 0 holds panels 0..K; about 16 chunks in all
-    const int64_t per = std::max<int64_t>(K + 1, cdiv(nbl_cols, 16)) * c->NB;
+    // chunks: K+1 single blocks, then 2, 3, 4, ... blocks up to 16.  A block's
+    // K updates take ~1.2x its copy (C2: 11.7 vs 10 ms), so chunks that grow
+    // by less than that keep the next chunk landing before the GPU needs it
+    // (equal ~16-block chunks left the GPU idle ~120 ms waiting for the first)
     std::vector<int64_t> cb;
-    for (int64_t x = 0; x < c->nloc; x += per) cb.push_back(x);
+    const int64_t lead = std::min<int64_t>(K + 1, nbl_cols);
+    for (int64_t x = 0; x < lead; ++x) cb.push_back(x * c->NB);
+    for (int64_t x = lead, sz = 2; x < nbl_cols; x += sz, sz = std::min<int64_t>(16, sz + 1))
+        cb.push_back(x * c->NB);
     cb.push_back(c->nloc);
     const int nc = (int)cb.size() - 1;
     int lo_p, hi_p;
@@ -435,6 +440,12 @@ hpl_status pipelined_start(hpl_ctx *c, const Arrival &a, int64_t *jstart)
     cudaStream_t st = c->s_la;
     const bool auto0 = c->leaf_auto;
     const int lmax0 = c->fw.leaf_max_ctas, lrows0 = c->fw.leaf_rows_per_cta, lwarp0 = c->fw.leaf_warp_ctas;
+    std::vector<int> applied(nc, 0);        // chunk k has received updates 0..applied[k]-1
+    int arrived = 0;                        // S_la waits for chunks [0, arrived)
+    auto arrive = [&](int k) -> hpl_status {
+        for (; arrived <= k; ++arrived) CK(c, cudaStreamWaitEvent(st, c->ev_arr[arrived], 0));
+        return HPL_OK;
+    };
     auto update = [&](int64_t j, int k) -> hpl_status {
         const int b = (int)(j % c->nbuf);
         const int64_t lo = std::max(lcols_before(c, j * c->NB + jb_of(c, j)), cb[k]);
@@ -444,26 +455,33 @@ hpl_status pipelined_start(hpl_ctx *c, const Arrival &a, int64_t *jstart)
         ST(rs_cols(c, st, j, b, lo, hi, SEC_RIGHT, &rs));
         return compute_cols(c, st, j, b, lo, hi, rs, true, true, c->timing);
     };
-    // chunk 0: FACT(0), then update(j) and FACT(j+1) for j < K — alone on the
-    // GPU, so the leaf gets every SM
+    // bring chunk k up to date through update upto-1
+    auto catch_up = [&](int k, int upto) -> hpl_status {
+        ST(arrive(k));
+        for (; applied[k] < upto; ++applied[k]) ST(update(applied[k], k));
+        return HPL_OK;
+    };
+    // FACT(0..K) — alone on the GPU, so the leaf gets every SM
     c->leaf_auto = false;
     fact_set_leaf_ctas(&c->fw, 0, 512);
     c->fw.leaf_warp_ctas = c->loop ? c->fw.max_ctas : 0;   // loopback: fact_panel
-    CK(c, cudaStreamWaitEvent(st, c->ev_arr[0], 0));
-    ST(fact_panel(c, st, 0, 0));
-    for (int64_t j = 0; j < K; ++j) {
-        ST(update(j, 0));
-        ST(fact_panel(c, st, j + 1, (int)((j + 1) % c->nbuf)));
+    for (int64_t j = 0; j <= K; ++j) {
+        if (c->mycol == (int)(j % c->Q)) {
+            // the chunk holding panel j's local columns, updated by 0..j-1
+            const int64_t lc = lcols_before(c, j * c->NB);
+            int k = 0;
+            while (cb[k + 1] <= lc) ++k;
+            ST(catch_up(k, (int)j));
+        }
+        ST(fact_panel(c, st, j, (int)(j % c->nbuf)));
     }
     c->leaf_auto = auto0;
     c->fw.leaf_max_ctas = lmax0;
     c->fw.leaf_rows_per_cta = lrows0;
     c->fw.leaf_warp_ctas = lwarp0;
     CK(c, cudaEventRecord(c->ev_panel[K % c->nbuf], st));
-    for (int k = 1; k < nc; ++k) {
-        CK(c, cudaStreamWaitEvent(st, c->ev_arr[k], 0));
-        for (int64_t j = 0; j < K; ++j) ST(update(j, k));
-    }
+    // every chunk: the rest of updates 0..K-1, in arrival order
+    for (int k = 0; k < nc; ++k) ST(catch_up(k, K));
     c->h2d_bytes = 8.0 * (double)c->mloc * (double)c->nloc;
     c->h2d_last = nc - 1;
     // the look-ahead loop continues from iteration K on the whole matrix
