@@ -230,8 +230,9 @@ hpl_status fact_panel(hpl_ctx *c, cudaStream_t st, int64_t j, int b, cudaEvent_t
         const int64_t j0 = j * c->NB, rows = c->mloc - lrows_before(c, j0);
         const int64_t ncols = c->nloc - lcols_before(c, j0);
         const double rest_ms = 2.0 * (double)rows * (double)ncols * c->NB / 35e12 * 1e3;
-        // FACT(0) has nothing to hide behind: it always gets every SM
-        const bool hide = j > 0 && rest_ms > c->leaf_hide_ms;
+        // FACT(0) has nothing to hide behind: it always gets every SM; nor
+        // has any FACT without look-ahead (the update before it is done)
+        const bool hide = c->lookahead && j > 0 && rest_ms > c->leaf_hide_ms;
         fact_set_leaf_ctas(&c->fw, hide ? c->leaf_few_ctas : 0, 512);
         c->fw.leaf_warp_ctas = hide ? c->leaf_warp : 0;
         // loopback: one-warp leaf CTAs only.  A 256-thread leaf CTA needs a
