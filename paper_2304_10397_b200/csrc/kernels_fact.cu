@@ -102,6 +102,40 @@ __device__ __forceinline__ double leaf_row_update(double *P, int64_t ldp, int k0
     return fabs(v[0]);
 }
 
+// Two rows (i0 and i1 = i0 + stride) at once: both rows' loads are issued
+// before either row's stores, twice the loads in flight per thread (a leaf
+// on few CTAs is bound by each SM's outstanding loads).  The arithmetic per
+// row is leaf_row_update's, so the bits are the same.
+__device__ __forceinline__ void leaf_row_update2(double *P, int64_t ldp, int k0, int w, int kk,
+                                                 int64_t i0, int64_t i1, double piv,
+                                                 const double *prow, double &n0, double &n1)
+{
+    const int kc = k0 + kk;
+    const double x0 = P[(int64_t)kc * ldp + i0], x1 = P[(int64_t)kc * ldp + i1];
+    double v0[LEAF_MAX], v1[LEAF_MAX];
+#pragma unroll
+    for (int c = 0; c < LEAF_MAX; ++c) {
+        const int cc = kk + 1 + c;
+        v0[c] = cc < w ? P[(int64_t)(k0 + cc) * ldp + i0] : 0.0;
+        v1[c] = cc < w ? P[(int64_t)(k0 + cc) * ldp + i1] : 0.0;
+    }
+    const double l0 = x0 / piv, l1 = x1 / piv;
+    P[(int64_t)kc * ldp + i0] = l0;
+    P[(int64_t)kc * ldp + i1] = l1;
+#pragma unroll
+    for (int c = 0; c < LEAF_MAX; ++c) {
+        const int cc = kk + 1 + c;
+        if (cc < w) {
+            v0[c] = fma(-l0, prow[cc], v0[c]);
+            v1[c] = fma(-l1, prow[cc], v1[c]);
+            P[(int64_t)(k0 + cc) * ldp + i0] = v0[c];
+            P[(int64_t)(k0 + cc) * ldp + i1] = v1[c];
+        }
+    }
+    n0 = fabs(v0[0]);
+    n1 = fabs(v1[0]);
+}
+
 // Leaf: right-looking GEPP of columns [k0, k0+w) of the panel (rows k0..m-1).
 // One grid barrier per column; the next column's local pivot candidate is
 // formed during the current column's update, so a column costs the barrier
@@ -221,7 +255,16 @@ leaf_fact_kernel(int m, int64_t ldp, double *P, int k0, int w, int64_t *ipiv, do
         // ---- 4. scale + rank-1 update of own rows > kc; next column's candidate
         bv = -1.0;
         br = LLONG_MAX;
-        for (int i = max(rbeg, kc + 1) + threadIdx.x; i < rend; i += NT) {
+        int i = max(rbeg, kc + 1) + threadIdx.x;
+        if (NT > 32) {
+            for (; i + NT < rend; i += 2 * NT) {
+                double n0, n1;
+                leaf_row_update2(P, ldp, k0, w, kk, i, i + NT, piv, s_prow, n0, n1);
+                if (kk + 1 < w && better(n0, i, bv, br)) { bv = n0; br = i; }
+                if (kk + 1 < w && better(n1, i + NT, bv, br)) { bv = n1; br = i + NT; }
+            }
+        }
+        for (; i < rend; i += NT) {
             const double nv = leaf_row_update(P, ldp, k0, w, kk, i, piv, s_prow);
             if (kk + 1 < w && better(nv, i, bv, br)) { bv = nv; br = i; }
         }
