@@ -129,7 +129,7 @@ struct hpl_ctx {
     bool leaf_auto = true;           // adaptive leaf grid (fact_panel)
     int leaf_few_ctas = 8;
     int leaf_warp = 0;               // >0: hidden FACT uses up to this many one-warp leaf CTAs
-    double leaf_hide_ms = 60.0;
+    double leaf_hide_ms = 15.0;
     bool timing = false;
     std::vector<cudaEvent_t> tev;   // 10 events per iteration when timing
     std::vector<double> timeline;   // 6 values per iteration (ms)
