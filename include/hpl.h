@@ -195,7 +195,11 @@ hpl_status hpl_set_timing(hpl_ctx *ctx, int32_t enable);
  *                          cluster with the leaf in shared memory
  *   leaf_variant 0|1|2 (0) P=1 FACT leaf: right-looking / left-looking / Crout
  *                          (bitwise-equal results)
- *   leaf_few_ctas, leaf_hide_ms, leaf_warp, leaf_ctas   leaf grid policy
+ *   leaf_few_ctas <n> (8), leaf_hide_ms <ms> (15), leaf_warp <n> (0), leaf_ctas <n>
+ *                          leaf grid policy: while the concurrent trailing DGEMM
+ *                          is estimated longer than leaf_hide_ms the leaf runs on
+ *                          leaf_few_ctas CTAs (or leaf_warp one-warp CTAs), else
+ *                          on every SM; leaf_ctas fixes the grid
  *   gemm_cfg -1|0|1|2 (-1) DGEMM tile config (128x64, 128x128, 64x64 = default)
  * Every knob is per context.  Unknown names return HPL_ERR_ARG.  On a multi-process context every rank
  * must set the same options before the same hpl_factor (the schedule decides
