@@ -662,7 +662,19 @@ leaf_fact_dist_kernel(int m, int64_t ldp, double *Pn, int k0, int w, int64_t *ip
         bv = -1.0;
         br = LLONG_MAX;
         const bool more = kk + 1 < w;
-        for (int r = max(rbeg, kc + 1) + threadIdx.x; r < rend; r += NT) {
+        int r = max(rbeg, kc + 1) + threadIdx.x;
+        if (NT > 32) {
+            for (; r + NT < rend; r += 2 * NT) {
+                double n0, n1;
+                leaf_row_update2(Pn, ldp, k0, w, kk, r, r + NT, piv, s_pay + k0, n0, n1);
+                if (more && (r >= jbp || dp.is_prow) && better(n0, r, bv, br)) { bv = n0; br = r; }
+                if (more && (r + NT >= jbp || dp.is_prow) && better(n1, r + NT, bv, br)) {
+                    bv = n1;
+                    br = r + NT;
+                }
+            }
+        }
+        for (; r < rend; r += NT) {
             const double nv = leaf_row_update(Pn, ldp, k0, w, kk, r, piv, s_pay + k0);
             if (more && (r >= jbp || dp.is_prow) && better(nv, r, bv, br)) { bv = nv; br = r; }
         }
