@@ -3,7 +3,8 @@
     DMMA chains, hplk_dmma_peak with blocks_per_sm x warps);
  2. the trailing DGEMM at the same m x n for k = 512 and 2048 (a CTA tile's
     mainloop grows with k, its prologue/epilogue do not) under the tile
-    configs and epilogue / persistence variants (cfg = 1000*red + 100*tpc + cfg).
+    configs (gemm_cfg 0/1/2; round 1's epilogue / persistence variants were
+    removed after measuring them, profiles/r01_gemm_*).
 
     python tools/gemm_overhead.py [m] [cfg ...]"""
 import json
@@ -14,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2304_10397_b200 as H  # noqa: E402
 
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-cfgs = [int(c) for c in sys.argv[2:]] or [2, 1002, 202, 402, 3, 4, 0]
+cfgs = [int(c) for c in sys.argv[2:]] or [2, 0, 1]
 peak = H.hplk_dmma_peak()
 for bps, w in ((1, 4), (1, 8), (1, 12), (3, 4), (1, 16), (2, 8), (4, 4)):
     tf = H.hplk_dmma_peak(20000, bps, w)
