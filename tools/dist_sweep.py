@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-DEFAULTS = dict(lookahead=1, leaf_few_ctas=8, leaf_hide_ms=60, split=0,
+DEFAULTS = dict(lookahead=1, leaf_few_ctas=8, leaf_hide_ms=15, split=0,
                 leaf_warp=0, leaf_cluster=1, leaf_variant=0)
 DIST_DEFAULTS = dict(rs_peer=1, lb_peer=1, fact_gather=65536, fact_gather_ms=8)
 
